@@ -1,0 +1,47 @@
+"""Init-time training (TOOL): LS fit of the 203-tap static equaliser and PILOT
+convergence of the adaptive taps, on a known training sequence.
+
+TEST / TOOL INFRASTRUCTURE ONLY (see oracle/kk_oracle.py header).
+
+PAPER l.53: "the 203-tap static frequency-domain equalizer is optimized offline
+using a training sequence every time that the data acquisition is initialized"
+and "after initial setup and convergence using a training sequence" (adaptive).
+Reading R4: the 203 taps are a centred complex FIR at 4 sps (tap i = -101..101)
+fitted by least squares so that x2 at the symbol instants (4-sps position 4n,
+reading R15) approximates the transmitted symbols.  The result is an INPUT of
+kk_rx_create (param `fir`) and is committed under data/fir/ by
+tools/make_fixtures.py, which calls only oracle/ (and synth/ for the input).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import kk_oracle as O
+
+
+def field_after_s3(window, left, p: O.RxParams):
+    """E_s for every whole Hilbert chunk of the window (oracle S1-S3)."""
+    pos0 = -left
+    a, l, _ = O.frontend(window, p.dc_offset, p.v_min)
+    j_first = -(-(pos0 + O.HILBERT_DISCARD) // O.HILBERT_HOP)
+    j_last = (pos0 + len(window) - (O.HILBERT_NFFT - O.HILBERT_DISCARD)) // O.HILBERT_HOP
+    phi = O.hilbert_phase(l, pos0, j_first, j_last)
+    e_pos0 = O.HILBERT_HOP * j_first
+    pos = np.arange(e_pos0, e_pos0 + len(phi), dtype=np.int64)
+    theta = O.tone_phase_fast(pos, p.tone_bin, p.buffer_len)
+    e_s = O.reconstruct_downconvert(a[pos - pos0], phi, O.carrier_amplitude(p.dc_offset, p.cspr_db), theta)
+    return e_s, e_pos0
+
+
+def train_fir(window, left, p: O.RxParams, symbols_tx, n_first, n_count, ridge=1e-9):
+    """min_h sum_n |sum_t h[t] E_s[4n + 101 - t] - s_n|^2 + ridge ||h||^2."""
+    e_s, e_pos0 = field_after_s3(window, left, p)
+    n = np.arange(n_first, n_first + n_count, dtype=np.int64)
+    t = np.arange(O.FIR_TAPS, dtype=np.int64)
+    idx = 4 * n[:, None] + O.FIR_HALF - t[None, :] - e_pos0
+    A = e_s[idx]
+    b = np.asarray(symbols_tx, dtype=np.complex128)
+    AhA = A.conj().T @ A
+    AhA += ridge * np.trace(AhA).real / O.FIR_TAPS * np.eye(O.FIR_TAPS)
+    h = np.linalg.solve(AhA, A.conj().T @ b)
+    return h

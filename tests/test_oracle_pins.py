@@ -1,0 +1,428 @@
+"""Pins of the float64 oracle against things other than itself (-m "not gpu").
+
+Each test names the paper passage / closed form / invariant it checks.  The
+oracle is only trusted after these pass (task rule 3).  A plausible mistake
+(wrong Hilbert sign, wrong downconversion sign, dropped 1/2 in the log, wrong
+tap index, transposed operand) fails at least one of them.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import constellation as C
+from oracle import kk_oracle as O
+from oracle import metrics as Mx
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_numbers.json")))
+
+
+# ---------------------------------------------------------------- S1 front end
+def test_frontend_constant_code():
+    """constant code c, offset d -> a = sqrt(c + d) everywhere;
+    l = ln a (the factor 1/2 of ln v is pinned here)."""
+    a, l, clip = O.frontend(np.full(100, 37, np.int16), np.float32(963.5))
+    assert np.all(a == math.sqrt(1000.5))
+    assert np.allclose(l, math.log(math.sqrt(1000.5)), rtol=0, atol=1e-15)
+    assert not clip.any()
+
+
+def test_frontend_clamp_and_count():
+    """Reading R9: code + d < v_min is clamped to v_min and counted."""
+    a, l, clip = O.frontend(np.array([-2048, 0, 5], np.int16), np.float32(10.0), v_min=1.0)
+    assert clip.tolist() == [True, False, False]
+    assert a[0] == 1.0 and l[0] == 0.0
+
+
+# ---------------------------------------------------------------- S2 Hilbert
+def _chunks_for(nsamp):
+    """positions [0, nsamp) with whole Hilbert windows inside."""
+    pos0 = 0
+    j_first = 1
+    j_last = (nsamp - 768) // 512
+    return pos0, j_first, j_last
+
+
+@pytest.mark.parametrize("k", [1, 7, 100, 255, 511])
+def test_hilbert_bin_centred_tone(k):
+    """H{cos} = sin exactly for a tone on the 1024-point grid (SPEC.md l.355,
+    PAPER l.47).  phi = -H{l} (reading R1) so phi = -sin.  The reference
+    argument is reduced with integers, so the only error is fp64 rounding."""
+    n = np.arange(8192)
+    psi = 0.3
+    arg = 2 * np.pi * ((k * n) % 1024) / 1024 + psi
+    l = np.cos(arg)
+    pos0, jf, jl = _chunks_for(len(n))
+    phi = O.hilbert_phase(l, pos0, jf, jl)
+    ref = -np.sin(arg[512 * jf:512 * (jl + 1)])
+    assert np.max(np.abs(phi - ref)) < 1e-12
+
+
+def test_hilbert_constant_and_nyquist_zero():
+    """Constant -> 0 (DC bin zeroed) and the Nyquist tone (-1)^n -> 0."""
+    n = np.arange(4096)
+    for l in (np.full(4096, 3.25), np.cos(np.pi * n)):
+        phi = O.hilbert_phase(l, 0, 1, 5)
+        assert np.max(np.abs(phi)) < 1e-12
+
+
+def test_hilbert_direct_form_closed_kernel():
+    """Direct circular convolution with the closed-form kernel of -i*sgn(k)
+    (DC, Nyquist zeroed): h[q] = (2/1024) cot(pi q / 1024) for odd q, 0 for even
+    q.  phi[512j + r] = -sum_m h[(256 + r - m) mod 1024] w_j[m]."""
+    rng = np.random.default_rng(5)
+    l = rng.standard_normal(4096)
+    phi = O.hilbert_phase(l, 0, 1, 5)
+    q = np.arange(1024)
+    h = np.zeros(1024)
+    odd = q % 2 == 1
+    h[odd] = 2.0 / 1024 / np.tan(np.pi * q[odd] / 1024)
+    for j in range(1, 6):
+        w = l[512 * j - 256:512 * j + 768]
+        for r in (0, 1, 255, 256, 511):
+            val = -np.sum(h[(256 + r - np.arange(1024)) % 1024] * w)
+            assert abs(val - phi[512 * (j - 1) + r]) < 1e-12
+
+
+def test_hilbert_blockwise_is_periodically_time_varying():
+    """The 1024/512 blockwise Hilbert is NOT the whole-buffer Hilbert (reported,
+    not gated): a shift by 512 commutes, a shift by 256
+    does not."""
+    rng = np.random.default_rng(1)
+    l = rng.standard_normal(8192)
+    a = O.hilbert_phase(l, 0, 2, 10)
+    b = O.hilbert_phase(np.roll(l, 512), 0, 3, 11)
+    assert np.max(np.abs(a - b)) < 1e-12
+    c = O.hilbert_phase(np.roll(l, 256), 0, 2, 10)
+    assert np.max(np.abs(np.roll(a, 256)[512:-512] - c[512:-512])) > 1e-3
+
+
+# ---------------------------------------------------------------- S3 reconstruction (exact MP field)
+def _exact_mp_field(n, amp, tone_bin, nbuf, seed=3, ntones=40, depth=0.25):
+    """E_tf = A exp(g), g a multitone on NEGATIVE bins of the 1024 grid, so
+    ln|E_tf| and arg E_tf are an exact circular Hilbert pair in every window.
+    Full field E = E_tf e^{+i theta} (tone above the signal).
+    Returns (E, s_true) with s_true = E - A e^{i theta}."""
+    rng = np.random.default_rng(seed)
+    ks = rng.choice(np.arange(1, 400), ntones, replace=False)
+    c = depth / ntones * (rng.standard_normal(ntones) + 1j * rng.standard_normal(ntones))
+    g = np.zeros(len(n), dtype=np.complex128)
+    for kk, cc in zip(ks, c):
+        g += cc * np.exp(-2j * np.pi * ((kk * n) % 1024) / 1024)
+    theta = 2 * np.pi * ((tone_bin * n) % nbuf) / nbuf
+    e_tf = amp * np.exp(g)
+    return e_tf * np.exp(1j * theta), (e_tf - amp) * np.exp(1j * theta)
+
+
+def test_exact_minimum_phase_field_recovered():
+    """KK exactness (PAPER l.47 S1-S3): for a strictly MP field
+    whose log-spectrum lies on the 1024 grid the blockwise chain recovers the
+    signal to fp64 rounding.  Also pins: the 1/2 in l = ln sqrt(v), the Hilbert
+    sign (reading R1), the e^{+i theta} downconversion and A_hat."""
+    nbuf = 1 << 14
+    tone_bin = 2113
+    amp = 7.0
+    n = np.arange(-2048, nbuf + 2048)
+    e, s_true = _exact_mp_field(n, amp, tone_bin, nbuf)
+    intensity = np.abs(e) ** 2
+    a, l, _ = O.frontend(intensity, 0.0, v_min=1e-12)
+    pos0 = -2048
+    jf, jl = -3, (nbuf + 2048 - 768) // 512
+    phi = O.hilbert_phase(l, pos0, jf, jl)
+    pos = np.arange(512 * jf, 512 * (jl + 1))
+    cspr = 10 * np.log10(amp ** 2 / 1.0)
+    d = amp ** 2 * (1 + 10 ** (cspr / 10)) / 10 ** (cspr / 10)   # so that A_hat == amp
+    a_hat = O.carrier_amplitude(d, cspr)
+    assert abs(a_hat - amp) < 1e-12
+    theta = O.tone_phase(pos, tone_bin, nbuf)
+    es = O.reconstruct_downconvert(a[pos - pos0], phi, a_hat, theta)
+    ref = s_true[pos - pos0]
+    rel = np.linalg.norm(es - ref) / np.linalg.norm(ref)
+    assert rel < 1e-10
+    # wrong Hilbert sign or wrong downconversion sign -> O(1) error
+    es_bad = O.reconstruct_downconvert(a[pos - pos0], -phi, a_hat, theta)
+    assert np.linalg.norm(es_bad - ref) / np.linalg.norm(ref) > 0.3
+    es_bad2 = O.reconstruct_downconvert(a[pos - pos0], phi, a_hat, -theta)
+    assert np.linalg.norm(es_bad2 - ref) / np.linalg.norm(ref) > 0.3
+
+
+def test_carrier_only_gives_zero():
+    """carrier-only input -> E_s = 0 after carrier removal."""
+    nbuf = 4096
+    n = np.arange(-1024, nbuf + 1024)
+    amp = 5.0
+    intensity = np.full(len(n), amp ** 2)
+    a, l, _ = O.frontend(intensity, 0.0)
+    phi = O.hilbert_phase(l, -1024, -1, 8)
+    pos = np.arange(-512, 4608)
+    es = O.reconstruct_downconvert(a[pos + 1024], phi, amp, O.tone_phase(pos, 17, nbuf))
+    assert np.max(np.abs(es)) < 1e-12
+
+
+def test_tone_phase_integer_reduction():
+    """theta_n is buffer-local: theta(n + N) == theta(n) exactly (reading R7),
+    and fast int64 path == exact Python-int path."""
+    nbuf = 1 << 22
+    pos = np.array([-17152, -1, 0, 1, 12345, nbuf - 1, nbuf, nbuf + 2303])
+    t1 = O.tone_phase(pos, 541065, nbuf)
+    t2 = O.tone_phase_fast(pos, 541065, nbuf)
+    assert np.array_equal(t1, t2)
+    assert O.tone_phase([nbuf + 5], 541065, nbuf)[0] == O.tone_phase([5], 541065, nbuf)[0]
+
+
+# ---------------------------------------------------------------- S4 static EQ + resample
+def _overlap_save_fold(e_s, h, nf, keep):
+    """Independent frequency-domain formulation (the method's 'pair of FFTs'):
+    window FFT, x H (h placed circularly), fold Z_k=(Y_k+Y_{k+nf/2})/2, nf/2 IFFT."""
+    H = np.zeros(nf, dtype=np.complex128)
+    for t, hv in enumerate(h):
+        H[(t - 101) % nf] += hv
+    H = np.fft.fft(H)
+    margin = (nf - keep) // 2
+    out = []
+    for start in range(margin, len(e_s) - keep - margin + 1, keep):
+        w = e_s[start - margin:start - margin + nf]
+        Y = np.fft.fft(w) * H
+        Z = 0.5 * (Y[:nf // 2] + Y[nf // 2:])
+        z = np.fft.ifft(Z)
+        out.append(z[margin // 2:margin // 2 + keep // 2])
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("nf,keep", [(1024, 768), (2048, 1536), (2048, 1792)])
+def test_static_eq_direct_equals_fold_overlap_save(nf, keep):
+    """Reading R5: the frequency-domain EQ with spectral fold is exact LTI
+    decimation of the 203-tap FIR, independent of the FFT size."""
+    rng = np.random.default_rng(7)
+    e_s = rng.standard_normal(8 * keep + nf) + 1j * rng.standard_normal(8 * keep + nf)
+    h = rng.standard_normal(203) + 1j * rng.standard_normal(203)
+    fs = _overlap_save_fold(e_s, h, nf, keep)
+    margin = (nf - keep) // 2
+    x2 = O.static_eq_resample(e_s, 0, h, margin // 2, len(fs))
+    assert np.max(np.abs(fs - x2)) < 1e-11 * np.max(np.abs(x2))
+
+
+def test_static_eq_impulse_response():
+    """E_s = delta at position 1000 -> x2[m] = h_{2m-1000} (tap index check)."""
+    e_s = np.zeros(4000, dtype=np.complex128)
+    e_s[1000] = 1.0
+    h = np.arange(203) + 1j * np.arange(203)[::-1]
+    x2 = O.static_eq_resample(e_s, 0, h, 400, 200)
+    for m in range(400, 600):
+        i = 2 * m - 1000
+        expect = h[i + 101] if -101 <= i <= 101 else 0
+        assert x2[m - 400] == expect
+
+
+# ---------------------------------------------------------------- S5 WL LMS
+def test_lms_mu_zero_passthrough():
+    """mu = 0, centre-spike taps -> taps unchanged, y = x2[2n]."""
+    pts, labs = C.make_standard("QAM16")
+    rng = np.random.default_rng(2)
+    x2 = rng.standard_normal(1000) + 1j * rng.standard_normal(1000)
+    w, g, _, _ = O.wl_lms_update(lambda m: x2[m], 10, 300, [0, 1, 0, 0], [0] * 4, 0.0, pts, 0.1, O.UPD_DD_SOFT)
+    assert np.array_equal(w, np.array([0, 1, 0, 0], complex)) and not g.any()
+    y = O.wl_apply(x2, 0, 10, 300, w, g)
+    assert np.array_equal(y, x2[20:620:2])
+
+
+def test_lms_pilot_converges_to_least_squares():
+    """PILOT mode (paper's training mode) on a noiseless linear +
+    conjugate mixing channel converges to the exact inverse (LS solution)."""
+    pts, labs = C.make_standard("QAM16")
+    rng = np.random.default_rng(4)
+    n_sym = 20000
+    pat = rng.integers(0, 16, n_sym)
+    s = pts[pat]
+    # x2 at 2 sps: symbol instants carry 0.9 e^{0.3i} s + 0.1 s*; half instants random
+    x2 = np.empty(2 * n_sym + 4, dtype=np.complex128)
+    x2[0::2][:n_sym] = 0.9 * np.exp(0.3j) * s + 0.1 * np.conj(s)
+    x2[1::2] = 0.05 * (rng.standard_normal(n_sym + 2) + 1j * rng.standard_normal(n_sym + 2))
+    x2_at = lambda m: x2[m + 2]  # noqa: E731
+    w, g, _, em = O.wl_lms_update(x2_at, 0, n_sym - 2, [0, 1, 0, 0], [0] * 4, 2e-2, pts, 0.0, O.UPD_PILOT, pat, 0)
+    y = O.wl_apply(x2, -2, 100, 1000, w, g)
+    assert np.max(np.abs(y - s[100:1100])) < 1e-3
+
+
+def test_lms_widely_linear_beats_strictly_linear():
+    """SPEC.md l.393 ablation: input x + 0.1 x* -> the WL taps cancel the
+    conjugate term; with g frozen at 0 the residual MSE is much higher."""
+    pts, labs = C.make_standard("QAM16")
+    rng = np.random.default_rng(6)
+    n_sym = 12000
+    pat = rng.integers(0, 16, n_sym)
+    s = pts[pat]
+    x2 = np.zeros(2 * n_sym + 4, dtype=np.complex128)
+    x2[0::2][:n_sym] = s + 0.1 * np.conj(s)
+    x2_at = lambda m: x2[m + 2]  # noqa: E731
+    w, g, _, _ = O.wl_lms_update(x2_at, 0, n_sym - 2, [0, 1, 0, 0], [0] * 4, 1e-2, pts, 0.0, O.UPD_PILOT, pat, 0)
+    mse_wl = np.mean(np.abs(O.wl_apply(x2, -2, 200, 2000, w, g) - s[200:2200]) ** 2)
+    # strictly linear optimum: best w only (g = 0): LS fit of w on the same data
+    xs = x2[0::2][200:2200]
+    wl = np.vdot(xs, s[200:2200]) / np.vdot(xs, xs)
+    mse_sl = np.mean(np.abs(wl * xs - s[200:2200]) ** 2)
+    assert mse_wl < 1e-6 and mse_sl > 1e-3
+
+
+def test_lms_soft_gate_lipschitz():
+    """Reading R10: with the soft gate a 1e-6 relative perturbation of x2 moves
+    the resulting taps by O(1e-6), so fp32 GPU taps stay close to
+    the fp64 oracle's; the gate fraction is in (0,1) for noisy data."""
+    pts, labs = C.make_standard("QAM64")
+    rng = np.random.default_rng(8)
+    n = 4096
+    s = pts[rng.integers(0, 64, n)]
+    x2 = np.zeros(2 * n + 4, dtype=np.complex128)
+    x2[0::2][:n] = s + 0.05 * (rng.standard_normal(n) + 1j * rng.standard_normal(n))
+    x2[1::2] = 0.1 * (rng.standard_normal(n + 2) + 1j * rng.standard_normal(n + 2))
+    tau = O.d_min(pts) ** 2 / 4
+    pert = x2 * (1 + 1e-6 * rng.standard_normal(len(x2)))
+    w1, g1, gated, _ = O.wl_lms_update(lambda m: x2[m + 2], 0, n - 2, [0, 1, 0, 0], [0] * 4, 1e-3, pts, tau, 0)
+    w2, g2, _, _ = O.wl_lms_update(lambda m: pert[m + 2], 0, n - 2, [0, 1, 0, 0], [0] * 4, 1e-3, pts, tau, 0)
+    assert np.max(np.abs(np.r_[w1 - w2, g1 - g2])) < 1e-5
+    assert 0 < gated < n
+
+
+# ---------------------------------------------------------------- S6 decisions
+def test_decide_exact_points_and_tie_break():
+    """y = p_k -> k; y = 0 on QAM4 (4-way tie) -> index 0."""
+    for name in C.STANDARD:
+        pts, _ = C.make_standard(name)
+        dec, margin = O.decide(pts, pts)
+        assert np.array_equal(dec, np.arange(len(pts)))
+        # exact point: distance to its cell boundary = half the nearest-neighbour distance
+        dd = np.abs(pts[:, None] - pts[None, :]) + np.eye(len(pts)) * 1e9
+        assert np.allclose(margin, dd.min(axis=1) / 2, rtol=0, atol=1e-12)
+    pts, _ = C.make_standard("QAM4")
+    dec, margin = O.decide(np.array([0j]), pts)
+    assert dec[0] == 0 and abs(margin[0]) < 1e-15
+
+
+def test_decide_margin_is_voronoi_distance():
+    """m_n = distance of y to the nearest Voronoi boundary: on a square grid it
+    is d_min/2 - max(|dx|, |dy|) for interior points (geometry, not the formula)."""
+    pts, _ = C.make_standard("QAM16")
+    dm = O.d_min(pts)
+    rng = np.random.default_rng(3)
+    inner = pts[np.abs(pts.real) < 0.5 * 3 * dm / 2][:1]
+    for _ in range(200):
+        k = rng.integers(len(pts))
+        off = (rng.uniform(-0.45, 0.45) + 1j * rng.uniform(-0.45, 0.45)) * dm
+        y = pts[k] + off
+        dec, m = O.decide(np.array([y]), pts)
+        assert dec[0] == k
+        # distance to the nearest boundary among the cell's existing neighbours
+        cand = []
+        for dx, dy in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+            nb = pts[k] + dm * complex(dx, dy)
+            if np.min(np.abs(pts - nb)) < 1e-9:
+                cand.append(dm / 2 - (off.real * dx + off.imag * dy))
+        assert abs(m[0] - min(cand)) < 1e-12
+    assert inner.size == 1
+
+
+def test_decide_random_vs_bruteforce_loop():
+    pts, _ = C.make_standard("QAM32")
+    rng = np.random.default_rng(9)
+    y = 1.3 * (rng.standard_normal(500) + 1j * rng.standard_normal(500))
+    dec, _ = O.decide(y, pts)
+    for yy, d in zip(y, dec):
+        best = min(range(len(pts)), key=lambda k: (abs(yy - pts[k]) ** 2, k))
+        assert best == d
+
+
+# ---------------------------------------------------------------- S7 counts
+def test_count_errors_basic():
+    """identical -> 0; one symbol wrong by a Gray neighbour -> 1 bit."""
+    pts, labs = C.make_standard("QAM16")
+    ref = np.arange(16)
+    r = O.count_errors(ref, ref, labs)
+    assert r["sym_errors"] == 0 and r["bit_errors"] == 0 and r["bits"] == 64
+    dec = ref.copy()
+    dec[0] = int(np.argmin(np.abs(pts - (pts[0] + O.d_min(pts))) + (np.arange(16) == 0) * 9))
+    r = O.count_errors(dec, ref, labs)
+    assert r["sym_errors"] == 1 and r["bit_errors"] == 1
+    r = O.count_errors(ref, (ref + 8) % 16, labs)
+    assert r["bit_errors"] == int(sum(bin(int(labs[i]) ^ int(labs[(i + 8) % 16])).count("1") for i in range(16)))
+
+
+# ---------------------------------------------------------------- constellations
+def test_constellation_invariants_and_gray():
+    """SPEC.md l.28-30 invariants; Gray labelling of square QAM (reading R12):
+    nearest neighbours differ in exactly one bit; QAM4 = (+-1 +-i)/sqrt2."""
+    for name in C.STANDARD:
+        p, l = C.make_standard(name)
+        C.validate(p, l)
+        assert abs(np.mean(np.abs(p) ** 2) - 1) < 1e-12
+    p, l = C.make_standard("QAM4")
+    assert np.allclose(sorted(p, key=lambda z: (z.real, z.imag)),
+                       np.array([-1 - 1j, -1 + 1j, 1 - 1j, 1 + 1j]) / np.sqrt(2))
+    for name in ("QAM4", "QAM16", "QAM64", "QAM8"):
+        p, l = C.make_standard(name)
+        dm = O.d_min(p)
+        for i in range(len(p)):
+            for j in range(len(p)):
+                if i != j and abs(abs(p[i] - p[j]) - dm) < 1e-9:
+                    assert bin(int(l[i]) ^ int(l[j])).count("1") == 1
+
+
+def test_cross_layout_geometry():
+    """32 = 6x6 minus 4 corners; 128 = 12x12 minus 16 corners (reading R12)."""
+    for name, side, ncorner in (("QAM32", 6, 4), ("QAM128", 12, 16)):
+        p, _ = C.make_standard(name)
+        g = np.round(p / (O.d_min(p) / 2)).astype(complex)
+        lv = sorted(set(g.real.astype(int)))
+        assert len(lv) == side and len(set(g.imag.astype(int))) == side
+        assert side * side - ncorner == len(set(np.round(g, 6)))
+
+
+def test_data_files_match_oracle(root):
+    """The committed data files (inputs shared by both sides) equal the oracle's
+    tables; GS files are valid and have GMI >= the conventional format."""
+    from oracle import shaping
+    for name in C.STANDARD:
+        p, l = C.load(os.path.join(root, "data", "constellations", name + ".txt"))
+        p0, l0 = C.make_standard(name)
+        assert np.max(np.abs(p - p0)) < 1e-14 and np.array_equal(l, l0)
+    for gs, base, snr in (("GS8", "QAM8", 14.0), ("GS128", "QAM128", 20.0)):
+        p, l = C.load(os.path.join(root, "data", "constellations", gs + ".txt"))
+        p0, l0 = C.make_standard(base)
+        order = 10 if len(p) <= 8 else 6
+        assert shaping.gmi_awgn(p, l, snr, order) > shaping.gmi_awgn(p0, l0, snr, order)
+
+
+# ---------------------------------------------------------------- metrics
+def test_q_thresholds_and_net_rates():
+    """PAPER l.83 thresholds <-> BER; PAPER l.103 net rates."""
+    fb = GOLD["fec_ber_derived"]
+    fq = GOLD["fec_q_db"]
+    for key in ("6.7%", "20%"):
+        assert abs(Mx.ber_from_q(fq[key]) / fb[key] - 1) < fb["tol_rel"]
+        assert abs(Mx.q_from_ber(Mx.ber_from_q(fq[key])) - fq[key]) < 1e-9
+    nr = GOLD["net_rate_gbps"]
+    assert round(Mx.net_throughput(64, 1.0, 0.20), 1) == nr["QAM64_20%"]
+    assert round(Mx.net_throughput(32, 1.0, 0.067), 1) == nr["QAM32_6.7%"]
+
+
+def test_closed_form_ber_reductions():
+    """Cho-Yoon reduces to Q(sqrt(SNR)) for 4-QAM and to
+    [3Q(x)+2Q(3x)-Q(5x)]/4, x = sqrt(SNR/5), for 16-QAM;
+    and matches a Monte-Carlo brute force for 64-QAM."""
+    for snr_db in (0.0, 6.0, 10.0):
+        s = 10 ** (snr_db / 10)
+        assert abs(Mx.ber_square_qam_gray(4, s) - Mx.qfunc(np.sqrt(s))) < 1e-15
+        x = np.sqrt(s / 5)
+        ref16 = (3 * Mx.qfunc(x) + 2 * Mx.qfunc(3 * x) - Mx.qfunc(5 * x)) / 4
+        assert abs(Mx.ber_square_qam_gray(16, s) / ref16 - 1) < 1e-12
+    pts, labs = C.make_standard("QAM64")
+    rng = np.random.default_rng(11)
+    snr = 10 ** (16 / 10)
+    n = 400000
+    idx = rng.integers(0, 64, n)
+    y = pts[idx] + np.sqrt(1 / snr / 2) * (rng.standard_normal(n) + 1j * rng.standard_normal(n))
+    dec, _ = O.decide(y, pts)
+    ber = O.count_errors(dec, idx, labs)["bit_errors"] / (6 * n)
+    th = Mx.ber_square_qam_gray(64, snr)
+    assert abs(ber - th) < 4 * np.sqrt(th / (6 * n)) + 0.02 * th
