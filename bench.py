@@ -1,0 +1,377 @@
+"""Throughput benchmark of the B200 KK receiver hot path (BASELINE.json metric).
+
+A step = one pass of the whole hot path (S1..S7: front end, Hilbert, reconstruct,
+static EQ + 4->2, LMS update pass, WL apply, decision, demap, count) over one
+batch of `--batch` 2^22-sample buffers of the C5 workload (GS-128, CSPR 16 dB,
+two-sided ASE at OSNR 35 dB) per GPU.  Inputs are resident in
+HBM (`value`); `e2e` repeats the measurement through the same C-ABI call with
+pinned HOST buffers (H2D of the batch + halos and D2H of the labels inside the
+timed region).
+
+  python bench.py [--gpus N --steps K --warmup W]            # this implementation
+  python bench.py --impl reference [--steps K --warmup W]    # the float64 CPU oracle
+  torchrun --nproc-per-node N bench.py --gpus N ...          # one rank per GPU (weak scaling)
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sustained GSa/s (equiv. GBaud) on full KK chain, 1/2/4/8 B200; % HBM roofline"
+UNIT = "GSa/s"
+# algorithmic work per ADC sample
+HBM_BYTES_PER_SA = 2.25          # int16 in + uint8 label per 4 samples out
+FLOP_PER_SA_X2 = 217.0           # kk_x2: Hilbert 100 + static EQ 97 + pointwise S1/S3 20
+FLOP_PER_SA_CHAIN = 240.0        # whole chain (+ WL apply 16, decision ~5, update ~0.2)
+# FP32 SIMT peak derived from the unit counts and max clock (B200_PROFILING.md):
+# 148 SMs x 128 FP32 lanes x 2 flop (FFMA) x 1.965 GHz
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[4:8]):
+                if v.strip().lower() in ("active", "1"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def load_fir(name):
+    h = np.loadtxt(os.path.join(ROOT, "data", "fir", f"{name}.txt"))
+    return h[:, 0] + 1j * h[:, 1]
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def profile_traffic():
+    """dram bytes per kk_x2 launch from the committed `ncu --set full` capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------
+# oracle (CPU) legs: cpu_baseline and --impl reference
+# ----------------------------------------------------------------------------
+def _oracle_one(args):
+    name, b, n_pool = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import kk_oracle as O
+    from synth import configs
+    from synth.generate import make_pool, make_stream
+    wl = configs.get(name)
+    cfg = wl.link
+    pool = make_pool(cfg, n_pool)
+    left, right = O.required_left(4096), 2304
+    st, off = make_stream(pool, 1, left, right, first=b)
+    p = O.RxParams(buffer_len=cfg.buffer_len, cspr_db=cfg.cspr_db, dc_offset=pool.dc_offset, fir=load_fir(name),
+                   points=pool.points, labels=pool.labels, tone_bin=cfg.tbin, pattern=pool.pattern)
+    t0 = time.perf_counter()
+    r = O.receive(st, off, p)
+    return time.perf_counter() - t0, r["bit_errors"], cfg.buffer_len
+
+
+def oracle_rate(name, n_pool, workers, tasks):
+    """Run `tasks` whole buffers through the oracle with `workers` processes.
+    Returns (GSa/s, seconds, samples)."""
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_oracle_one, [(name, b % n_pool, n_pool) for b in range(tasks)])
+    dt = time.perf_counter() - t0
+    samples = sum(r[2] for r in res)
+    return samples / dt / 1e9, dt, samples
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    workers = min(os.cpu_count() or 1, args.ref_workers)
+    from synth import configs
+    from synth.generate import make_pool
+    make_pool(configs.get(args.workload).link, args.pool)  # warm the input cache outside the timed steps
+    for _ in range(args.warmup):
+        oracle_rate(args.workload, args.pool, workers, workers)
+    times, samples = [], 0
+    for _ in range(args.steps):
+        _, dt, s = oracle_rate(args.workload, args.pool, workers, workers)
+        times.append(dt)
+        samples += s
+    total = sum(times)
+    value = samples / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload + " (GS-128 CSPR 16 dB two-sided OSNR 35 dB, 2^22-sample buffers)",
+                   "buffers_per_step": workers, "l2": "inputs > L2 not applicable (CPU)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle",
+                         "sample": f"{workers} whole 2^22-sample buffers per step, one per process"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# GPU leg
+# ----------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    from synth import configs
+    from synth.generate import make_pool, make_stream
+
+    wl = configs.get(args.workload)
+    cfg = wl.link
+    N = cfg.buffer_len
+    B = args.batch
+    P = args.pool
+    # rank 0 generates (and caches) the pool first, then the others load it
+    if rank == 0:
+        pool = make_pool(cfg, P)
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        pool = make_pool(cfg, P)
+    fir = load_fir(args.workload)
+    left, right = halo_for(N)
+    # device-resident stream: pool cycled so every step's B buffers + halos are contiguous
+    span = P + B
+    stream_np, off = make_stream(pool, span, left, right, first=0)
+    d_stream = torch.from_numpy(stream_np).to(dev)
+    d_out = torch.empty(B * (N // 4), dtype=torch.uint8, device=dev)
+    cur = torch.cuda.current_stream(dev)
+    rx = KKReceiver("CUSTOM" if not cfg.fmt.startswith("QAM") else cfg.fmt, N, cfg.cspr_db, fir, pool.dc_offset,
+                    points=pool.points, labels=pool.labels, tone_bin=cfg.tbin, ref_pattern=pool.pattern,
+                    device=local, stream=cur.cuda_stream, max_batch=B)
+
+    def first_buf(step):
+        # weak scaling: rank r walks the pool from its own offset
+        return (rank * B + step * B * world) % P
+
+    def step_dev(s):
+        b0 = first_buf(s)
+        rx.seek(b0)
+        return rx.process_batch(d_stream, off + b0 * N, B, d_out)
+
+    for s in range(args.warmup):
+        step_dev(s)
+    torch.cuda.synchronize(dev)
+    rx.set_timing(True)
+    counts = []
+    launches = 0
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        t0.record(cur)
+        for s in range(args.steps):
+            counts += step_dev(args.warmup + s)
+            launches += rx.last_launches()
+        t1.record(cur)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    ktimes = rx.kernel_times()
+    rx.set_timing(False)
+    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
+    agg = torch.tensor([sum(c["bit_errors"] for c in counts), sum(c["bits"] for c in counts),
+                        sum(c["sym_errors"] for c in counts), sum(c["symbols"] for c in counts)],
+                       dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(agg, op=dist.ReduceOp.SUM)
+    ms_max = float(tmax.item())
+    samples_total = world * args.steps * B * N
+    value = samples_total / (ms_max / 1e3) / 1e9
+
+    # ---------------- e2e through the same C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_stream = torch.from_numpy(stream_np).pin_memory()
+        h_out = torch.empty(B * (N // 4), dtype=torch.uint8).pin_memory()
+
+        def step_host(s):
+            b0 = first_buf(s)
+            rx.seek(b0)
+            return rx.process_batch(h_stream, off + b0 * N, B, h_out)
+
+        step_host(0)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        for s in range(args.steps):
+            step_host(s)
+        e1.record(cur)
+        torch.cuda.synchronize(dev)
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        h2d = (left + B * N + right) * 2
+        d2h = B * (N // 4) + B * 64
+        e2e = {"value": samples_total / (float(et.item()) / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    if rank != 0:
+        rx.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    x2_ms, x2_n = ktimes["kk_x2"]
+    x2_avg_ms = x2_ms / max(x2_n, 1)
+    x2_flops = FLOP_PER_SA_X2 * B * N
+    achieved_tf = x2_flops / (x2_avg_ms / 1e3) / 1e12
+    traffic = profile_traffic()
+    step_ms = ms_max / args.steps
+    lms_avg = ktimes["kk_lms"][0] / max(ktimes["kk_lms"][1], 1)
+    app_avg = ktimes["kk_apply"][0] / max(ktimes["kk_apply"][1], 1)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: GS-128, CSPR 16 dB, two-sided ASE at OSNR 35 dB, "
+                               f"2^22-sample 12-bit buffers, {B} buffers/step/GPU, pool of {P} distinct buffers "
+                               f"cycled (inputs+x2 scratch > L2 per step)",
+                   "buffer_len": N, "buffers_per_step_per_gpu": B, "parallelism": f"buffer-sharded x{world}",
+                   "l2": "inputs larger than L2 (pool %.0f MiB + x2 scratch %.0f MiB per step)" % (
+                       P * N * 2 / 2**20, B * N / 2 * 8 / 2**20)},
+        "gbaud_equiv": value / 4.0,
+        "hbm_fraction": value * HBM_BYTES_PER_SA / hbm,
+        "fp32_fraction_chain": value * FLOP_PER_SA_CHAIN / (FP32_PEAK_TFLOPS * 1e3),
+        "roofline": {"bound": "alu", "kernel": "kk_x2", "achieved": achieved_tf, "peak": FP32_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved_tf / FP32_PEAK_TFLOPS,
+                     "traffic": (traffic or {}).get("kk_x2_bytes_per_launch_scaled", None) if traffic else None,
+                     "flop_per_sa": FLOP_PER_SA_X2, "avg_launch_ms": x2_avg_ms,
+                     "peak_basis": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (derived, DESIGN.md)"},
+        "kernel_ms_per_step": {"kk_x2": x2_avg_ms, "kk_lms": lms_avg, "kk_apply": app_avg},
+        "errors": {"bit_errors": int(agg[0]), "bits": int(agg[1]), "ber": int(agg[0]) / max(int(agg[1]), 1)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        workers = min(os.cpu_count() or 1, args.ref_workers)
+        v, dt, s = oracle_rate(args.workload, P, workers, workers)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": workers, "kind": "oracle",
+                                "sample": f"{workers} whole 2^22-sample C5 buffers, one per process ({dt:.1f} s)"}
+    print(json.dumps(line), flush=True)
+    rx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kk", choices=["kk", "reference"])
+    ap.add_argument("--workload", default="C5")
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--pool", type=int, default=16)
+    ap.add_argument("--ref-workers", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: W >= 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

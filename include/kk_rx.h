@@ -1,0 +1,184 @@
+/*
+ * kk_rx.h -- C ABI of the B200-native Kramers-Kronig receiver hot path.
+ *
+ * One call processes raw 12-bit ADC buffers (int16 codes) into symbol decisions,
+ * demapped labels and error counts, following the real-time DSP chain of
+ * arXiv 2108.07004, Sec. 2:
+ *
+ *   S1 fixed->float, + DC offset, sqrt, log          PAPER l.47 ("first kernel")
+ *   S2 blockwise 1024-pt Hilbert (keep centre 512)    PAPER l.47 ("step 3")
+ *   S3 a*e^{i phi}, carrier removal, downconversion
+ *   S4 203-tap static EQ + 4->2 sps resampling
+ *   S5 4-tap widely-linear LMS (update pass + apply)
+ *   S6 minimum-Euclidean-distance decision
+ *   S7 demap to labels ("bits to RAM") + counting
+ *
+ * Readings of the paper where it is silent are listed in DESIGN.md (R1..R17).
+ * All functions are thread-compatible: one handle per host thread.
+ *
+ * Errors: every function returns kk_status.  KK_EINVAL for bad arguments,
+ * KK_ENOMEM for allocation failure, KK_ECUDA for a CUDA runtime error (sticky:
+ * the handle must be destroyed), KK_ESTATE for calls in the wrong order,
+ * KK_EUNSUPPORTED for unsupported configurations.  kk_rx_last_error() returns
+ * a human-readable message for the last failure on the calling thread.
+ * Data-domain problems are never errors: code + d < v_min is clamped and
+ * counted (clipped_samples); a diverging adaptive equaliser sets a flag bit.
+ */
+#ifndef KK_RX_H
+#define KK_RX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KK_RX_ABI_VERSION 1
+
+typedef struct kk_rx kk_rx_t; /* opaque: owns device scratch, tables, streams */
+
+typedef enum {
+  KK_OK = 0,
+  KK_EINVAL = -1,
+  KK_ENOMEM = -2,
+  KK_ECUDA = -3,
+  KK_ESTATE = -4,
+  KK_EUNSUPPORTED = -5
+} kk_status;
+
+/* Modulation formats.  GS8 / GS128 / CUSTOM need `points` and
+ * `labels` in kk_rx_params (the paper uploads them, l.53); the conventional
+ * formats are built in (Gray square QAM, 4x2 rectangular 8-QAM, cross 32/128;
+ * reading R12) unless `points` overrides them. */
+typedef enum {
+  KK_QAM4 = 0, KK_QAM8 = 1, KK_QAM16 = 2, KK_QAM32 = 3, KK_QAM64 = 4, KK_QAM128 = 5,
+  KK_GS8 = 6, KK_GS128 = 7, KK_CUSTOM = 8
+} kk_format;
+
+/* Reference of the adaptive-equaliser update (reading R10).
+ * DD_SOFT: decision-directed with the soft gate gamma = min(1,(D2-D1)/tau) (default)
+ * PILOT  : the known pattern symbol (the paper's training mode)
+ * DD_HARD: textbook decision-directed (gamma = 1). */
+typedef enum { KK_UPD_DD_SOFT = 0, KK_UPD_PILOT = 1, KK_UPD_DD_HARD = 2 } kk_update_mode;
+
+#define KK_DUMP_ES 1u /* keep E_s (after S3) of the last call for kk_rx_debug_es() */
+
+typedef struct {
+  float dc_offset;          /* d, ADC-code units, added before sqrt/log */
+  int64_t tone_bin;         /* tone frequency = tone_bin * fs / buffer_len; default 541065 */
+  const float *fir;         /* REQUIRED: 2*fir_len floats (re,im interleaved), tap i = index-101, 4 sps */
+  int32_t fir_len;          /* must be 203 */
+  const float *w_init;      /* 16 floats: w[0..3] then g[0..3], complex interleaved; NULL = w=(0,1,0,0), g=0 */
+  float mu;                 /* LMS step, default 1e-3 */
+  int32_t k_update;         /* K: LMS steps per sub-block update pass, default 4096 */
+  int32_t sub_block;        /* L: symbols per fixed-tap sub-block; 0 = buffer_len/sps (default) */
+  float gate_tau;           /* tau of the soft gate; < 0 => d_min^2/4 (default); 0 => hard */
+  int32_t update_mode;      /* kk_update_mode */
+  const float *points;      /* 2*m floats (re,im), or NULL for the built-in table of `fmt` */
+  const uint8_t *labels;    /* m bit labels, a permutation of 0..m-1 */
+  int32_t m;                /* number of points (4..128, power of two) */
+  const uint8_t *ref_pattern; /* error-count / PILOT reference: point INDICES, length ref_len; NULL = no counting */
+  int32_t ref_len;          /* P, pattern period in symbols (2^20 in the paper) */
+  int64_t ref_offset;       /* pattern index of symbol 0 of stream buffer 0 */
+  float v_min;              /* clamp floor of code + d, default 1.0 (one LSB) */
+  int32_t device;           /* CUDA device ordinal, -1 = current */
+  void *cuda_stream;        /* cudaStream_t to launch on, NULL = handle-owned stream */
+  uint32_t debug_dump;      /* bitmask of KK_DUMP_* */
+  int32_t max_batch;        /* buffers per internal batch (device scratch sizing), default 16 */
+} kk_rx_params;
+
+/* Per-buffer (or aggregate) counters, "Error counting". */
+typedef struct {
+  uint64_t bit_errors;      /* sum popcount(label[d_n] ^ label[ref_n]) */
+  uint64_t sym_errors;      /* #(d_n != ref_n) */
+  uint64_t bits;            /* symbols * log2(m) (0 when no ref_pattern) */
+  uint64_t symbols;         /* buffer_len / sps per buffer */
+  uint64_t clipped_samples; /* samples with code + d < v_min (clamped) */
+  uint64_t gated_updates;   /* LMS steps whose soft gate was < 1 */
+  uint32_t flags;           /* bit 0: adaptive equaliser diverged (mean |e|^2 > 1 or non-finite taps) */
+  uint32_t reserved;
+} kk_rx_counts;
+
+/* Fill *p with defaults (tone_bin 541065, mu 1e-3, K 4096, L 0, tau -1,
+ * DD_SOFT, v_min 1, device -1, max_batch 16; pointers NULL).  Host only. */
+void kk_rx_params_default(kk_rx_params *p);
+
+/* Create a receiver.  fmt: kk_format; sps must be 4 (4 -> 2);
+ * buffer_len: samples per buffer (2^22 in the paper), multiple of 512,
+ * >= 4*k_update + 3200, <= 2^30; cspr_db: carrier-to-signal power ratio used
+ * for carrier removal A_hat = sqrt(d c/(1+c)) (reading R6).
+ * Copies every table it needs from *p (the caller may free them after).
+ * Allocates device memory on p->device.  Errors: KK_EINVAL (bad params),
+ * KK_ENOMEM, KK_ECUDA (no device). */
+kk_status kk_rx_create(kk_rx_t **out, int fmt, int sps, int64_t buffer_len, float cspr_db,
+                       const kk_rx_params *p);
+
+/* Samples that must be readable before the first and after the last sample of
+ * the buffers passed to kk_rx_process*.  Outputs of buffer b depend only on
+ * raw samples [b*N - left, (b+1)*N + right). */
+kk_status kk_rx_halo(const kk_rx_t *h, int64_t *left, int64_t *right);
+
+/* Same, without a handle (host only; for sizing and tests). */
+kk_status kk_rx_halo_for(int64_t buffer_len, int32_t k_update, int64_t *left, int64_t *right);
+
+/* Process one buffer.  `buffer` points at its first sample inside a contiguous
+ * caller-owned stream (device or host memory; halos readable).  out_symbols:
+ * buffer_len/4 bytes (device or host), each the bit label of the decided point
+ * ("demapped into bits").  out_errors: host struct, may be NULL.
+ * Returns when the outputs are valid.  Advances the stream position by one
+ * buffer (pattern offset for error counting). */
+kk_status kk_rx_process(kk_rx_t *h, const int16_t *buffer, uint8_t *out_symbols, kk_rx_counts *out_errors);
+
+/* Process nbuf consecutive buffers starting at `first` (contiguous stream).
+ * out_symbols: nbuf*buffer_len/4 bytes or NULL; out_per_buf: nbuf host structs
+ * or NULL.  Internally batched (max_batch) and pipelined: with host input the
+ * copy of batch j+1 overlaps the compute of batch j. */
+kk_status kk_rx_process_batch(kk_rx_t *h, const int16_t *first, int64_t nbuf, uint8_t *out_symbols,
+                              kk_rx_counts *out_per_buf);
+
+/* Set the stream index of the next buffer (pattern offset = ref_offset +
+ * index*buffer_len/4 mod ref_len).  Default after create: 0. */
+kk_status kk_rx_seek(kk_rx_t *h, int64_t buffer_index);
+
+/* Adaptive taps used for buffer `buf` (0-based) of the LAST internal batch of
+ * the last call: 16 floats (w[4], g[4] complex) per sub-block, all sub-blocks. */
+kk_status kk_rx_get_taps(kk_rx_t *h, int64_t buf, float *out);
+
+/* Running totals since create / kk_rx_reset_totals. */
+kk_status kk_rx_totals(const kk_rx_t *h, kk_rx_counts *out);
+kk_status kk_rx_reset_totals(kk_rx_t *h);
+
+/* Debug (parity tests): x2 (S4 output, 2 sps) of the last internal batch,
+ * x2 index relative to that batch's first buffer (x2 index m <-> 4-sps position
+ * 2m); valid range [-(2*k_update+2), nbuf*buffer_len/2).  2*count floats. */
+kk_status kk_rx_debug_x2(kk_rx_t *h, int64_t first, int64_t count, float *out);
+
+/* Debug: E_s (S3 output, 4 sps) of the last internal batch (needs
+ * KK_DUMP_ES at create), positions [0, nbuf*buffer_len). 2*count floats. */
+kk_status kk_rx_debug_es(kk_rx_t *h, int64_t first, int64_t count, float *out);
+
+/* Built-in constellation table (host only): 2*m floats, m labels. Returns m or <0. */
+int kk_rx_constellation(int fmt, float *points_out, uint8_t *labels_out);
+
+/* Number of kernel launches issued by the last process call (for the bench). */
+int64_t kk_rx_last_launches(const kk_rx_t *h);
+
+/* Per-kernel device timing (CUDA events recorded on the launch stream around
+ * each kernel of every internal batch).  kk_rx_set_timing(h, 1) enables and
+ * resets; kk_rx_kernel_times returns accumulated milliseconds and launch
+ * counts for {kk_x2, kk_lms, kk_apply} (3 entries each). */
+kk_status kk_rx_set_timing(kk_rx_t *h, int on);
+kk_status kk_rx_kernel_times(const kk_rx_t *h, double *ms_out, int64_t *n_out);
+
+/* Message for the last failure on this thread (never NULL). */
+const char *kk_rx_last_error(const kk_rx_t *h);
+
+/* Free everything; NULL is a no-op. */
+kk_status kk_rx_destroy(kk_rx_t *h);
+
+int kk_rx_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KK_RX_H */

@@ -1,0 +1,625 @@
+// kk_rx.cu -- C ABI (include/kk_rx.h) of the B200-native KK receiver.
+//
+// Host side: argument validation, constellation / static-EQ / twiddle tables
+// (fp64, rounded once to fp32), device scratch, streams and the per-batch
+// launch sequence  kk_x2_kernel -> kk_lms_kernel -> kk_apply_kernel.
+// With host input the H2D of batch j+1 (copy stream) overlaps the kernels of
+// batch j (compute stream), double-buffered device staging.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kk_rx.h"
+#include "kk_internal.h"
+
+namespace kk {
+int builtin_constellation(int fmt, std::vector<double>& pts, std::vector<int>& labs);
+}
+
+using namespace kk;
+
+namespace {
+thread_local std::string g_err = "";
+
+kk_status fail(kk_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+}  // namespace
+
+struct kk_rx {
+  int device = 0;
+  int64_t N = 0, n_sym = 0, L = 0;
+  int nsub = 0, K = 0, m = 0, bits_per = 0, max_batch = 16;
+  int64_t left = 0, right = 0;
+  int steps_per_buf = 0, pre_first = 0, pre_steps = 0;
+  int64_t x2h = 0;
+  float dc = 0, vmin = 1, a_hat = 0, mu = 1e-3f, tau = 0;
+  int mode = 0;
+  uint32_t tb_mod = 0, s32 = 0, s512 = 0;
+  int64_t P = 0, ref_offset = 0, stream_index = 0;
+  bool has_pattern = false;
+  uint32_t dump = 0;
+  int grid_x2 = 0;
+  // device
+  float2 *d_tw = nullptr, *d_tw512 = nullptr, *d_H = nullptr, *d_pts = nullptr, *d_winit = nullptr;
+  uint8_t *d_lab = nullptr, *d_pattern = nullptr;
+  float2* d_x2buf = nullptr;  // x2 index -x2h .. max_batch*N/2
+  float2* d_taps = nullptr;
+  unsigned long long* d_counts = nullptr;
+  uint8_t* d_out = nullptr;
+  int16_t* d_stage[2] = {nullptr, nullptr};
+  float2* d_es = nullptr;
+  unsigned long long* h_counts = nullptr;  // pinned
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  kk_rx_counts totals{};
+  kk_status sticky = KK_OK;
+  int last_nb = 0;
+  int64_t last_launches = 0;
+  // per-kernel timing (kk_rx_set_timing): events around each kernel of a batch
+  bool timing = false;
+  cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
+  double kernel_ms[3] = {0, 0, 0};
+  int64_t kernel_n[3] = {0, 0, 0};
+};
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess) {                                                            \
+      if (h) h->sticky = KK_ECUDA;                                                      \
+      return fail(KK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));        \
+    }                                                                                   \
+  } while (0)
+
+static void halo_geometry(int64_t N, int K, int64_t* left, int64_t* right, int* spb, int* i0, int64_t* x2h) {
+  const int64_t X2H = 2 * (int64_t)K + 64;
+  const int steps = (int)((N + 125) / STEP) + 1;
+  int64_t num = N - 2 * X2H - 2944;
+  int first = (num >= 0) ? (int)(num / STEP) + 1 : 0;
+  if (first > steps) first = steps;
+  // GPU grid needs: warm-up window of the first pre-pass step, last step window
+  const int64_t gpu_left = N - ((int64_t)STEP * first - 1280);
+  const int64_t gpu_right = (int64_t)STEP * steps + 256 - N;
+  // method needs (oracle window): 512*ceil((4K+4+101)/512) + 256 and 768
+  const int64_t need = 4 * (int64_t)K + 4 + 101;
+  const int64_t m_left = 512 * ((need + 511) / 512) + 256;
+  *left = std::max(gpu_left, m_left);
+  *right = std::max<int64_t>(gpu_right, 768);
+  if (spb) *spb = steps;
+  if (i0) *i0 = first;
+  if (x2h) *x2h = X2H;
+}
+
+extern "C" {
+
+int kk_rx_abi_version(void) { return KK_RX_ABI_VERSION; }
+
+void kk_rx_params_default(kk_rx_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->tone_bin = 541065;
+  p->fir_len = 203;
+  p->mu = 1e-3f;
+  p->k_update = 4096;
+  p->sub_block = 0;
+  p->gate_tau = -1.0f;
+  p->update_mode = KK_UPD_DD_SOFT;
+  p->v_min = 1.0f;
+  p->device = -1;
+  p->max_batch = 16;
+}
+
+const char* kk_rx_last_error(const kk_rx_t*) { return g_err.c_str(); }
+
+int kk_rx_constellation(int fmt, float* points_out, uint8_t* labels_out) {
+  std::vector<double> pts;
+  std::vector<int> labs;
+  const int m = builtin_constellation(fmt, pts, labs);
+  if (m < 0) {
+    g_err = "format has no built-in table";
+    return -1;
+  }
+  if (points_out)
+    for (int k = 0; k < 2 * m; ++k) points_out[k] = (float)pts[k];
+  if (labels_out)
+    for (int k = 0; k < m; ++k) labels_out[k] = (uint8_t)labs[k];
+  return m;
+}
+
+kk_status kk_rx_halo_for(int64_t buffer_len, int32_t k_update, int64_t* left, int64_t* right) {
+  if (!left || !right || buffer_len <= 0 || k_update <= 0) return fail(KK_EINVAL, "bad arguments");
+  halo_geometry(buffer_len, k_update, left, right, nullptr, nullptr, nullptr);
+  return KK_OK;
+}
+
+kk_status kk_rx_destroy(kk_rx_t* h) {
+  if (!h) return KK_OK;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+  void* ptrs[] = {h->d_tw, h->d_tw512, h->d_H, h->d_pts, h->d_winit, h->d_lab, h->d_pattern, h->d_x2buf,
+                  h->d_taps, h->d_counts, h->d_out, h->d_stage[0], h->d_stage[1], h->d_es};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h->h_counts) cudaFreeHost(h->h_counts);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
+    if (h->ev_used[i]) cudaEventDestroy(h->ev_used[i]);
+  }
+  for (int i = 0; i < 4; ++i)
+    if (h->ev_t[i]) cudaEventDestroy(h->ev_t[i]);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  cudaSetDevice(cur);
+  return KK_OK;
+}
+
+kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, float cspr_db, const kk_rx_params* p) {
+  if (!out || !p) return fail(KK_EINVAL, "out and params are required");
+  *out = nullptr;
+  if (sps != 4) return fail(KK_EINVAL, "sps must be 4 (PAPER l.47: 4 -> 2 samples per symbol)");
+  if (buffer_len <= 0 || buffer_len % 512 != 0 || buffer_len > (1LL << 30))
+    return fail(KK_EINVAL, "buffer_len must be a positive multiple of 512 and <= 2^30");
+  if (!p->fir || p->fir_len != 203) return fail(KK_EINVAL, "fir with fir_len == 203 is required (PAPER l.53)");
+  if (p->k_update <= 0) return fail(KK_EINVAL, "k_update must be > 0");
+  if (buffer_len < 4 * (int64_t)p->k_update + 3200)
+    return fail(KK_EINVAL, "buffer_len must be >= 4*k_update + 3200");
+  const int64_t n_sym = buffer_len / 4;
+  const int64_t L = p->sub_block > 0 ? p->sub_block : n_sym;
+  if (n_sym % L != 0) return fail(KK_EINVAL, "sub_block must divide buffer_len/4");
+  if (p->update_mode < 0 || p->update_mode > 2) return fail(KK_EINVAL, "bad update_mode");
+  if (p->update_mode == KK_UPD_PILOT && !p->ref_pattern) return fail(KK_EINVAL, "PILOT mode needs ref_pattern");
+  if (!(cspr_db > -100.f && cspr_db < 100.f)) return fail(KK_EINVAL, "bad cspr_db");
+  if (!(p->dc_offset > 0.f)) return fail(KK_EINVAL, "dc_offset must be > 0");
+  if (!(p->v_min > 0.f)) return fail(KK_EINVAL, "v_min must be > 0");
+  if (p->max_batch < 0) return fail(KK_EINVAL, "max_batch must be >= 0");
+
+  // constellation
+  std::vector<double> pts;
+  std::vector<int> labs;
+  int m = 0;
+  if (p->points) {
+    if (!p->labels || p->m < 4 || p->m > 128 || (p->m & (p->m - 1)))
+      return fail(KK_EINVAL, "points need labels and a power-of-two m in [4,128]");
+    m = p->m;
+    pts.resize(2 * m);
+    labs.resize(m);
+    for (int k = 0; k < 2 * m; ++k) pts[k] = p->points[k];
+    for (int k = 0; k < m; ++k) labs[k] = p->labels[k];
+  } else {
+    if (fmt == KK_GS8 || fmt == KK_GS128 || fmt == KK_CUSTOM)
+      return fail(KK_EINVAL, "GS / custom formats need points and labels (PAPER l.53: uploaded)");
+    m = builtin_constellation(fmt, pts, labs);
+    if (m < 0) return fail(KK_EINVAL, "unknown format");
+  }
+  if ((fmt == KK_GS8 && m != 8) || (fmt == KK_GS128 && m != 128)) return fail(KK_EINVAL, "m does not match format");
+  {
+    std::vector<int> seen(m, 0);
+    for (int k = 0; k < m; ++k) {
+      if (labs[k] < 0 || labs[k] >= m || seen[labs[k]]) return fail(KK_EINVAL, "labels must be a permutation");
+      seen[labs[k]] = 1;
+    }
+  }
+  double dmin2 = 1e300;
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j)
+      if (i != j) {
+        const double dx = pts[2 * i] - pts[2 * j], dy = pts[2 * i + 1] - pts[2 * j + 1];
+        dmin2 = std::min(dmin2, dx * dx + dy * dy);
+      }
+  if (!(dmin2 > 0)) return fail(KK_EINVAL, "duplicate constellation points");
+  if (p->ref_pattern) {
+    if (p->ref_len <= 0) return fail(KK_EINVAL, "ref_len must be > 0");
+    for (int64_t i = 0; i < p->ref_len; ++i)
+      if (p->ref_pattern[i] >= m) return fail(KK_EINVAL, "ref_pattern holds indices >= m");
+  }
+
+  kk_rx* h = new kk_rx();
+  int dev = p->device;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      delete h;
+      return fail(KK_ECUDA, "no CUDA device");
+    }
+  }
+  h->device = dev;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cudaSetDevice(dev) != cudaSuccess) {
+    delete h;
+    return fail(KK_ECUDA, "cudaSetDevice failed");
+  }
+  struct Restore {
+    int d;
+    ~Restore() { cudaSetDevice(d); }
+  } restore{cur};
+
+  h->N = buffer_len;
+  h->n_sym = n_sym;
+  h->L = L;
+  h->nsub = (int)(n_sym / L);
+  h->K = p->k_update;
+  h->m = m;
+  h->bits_per = 0;
+  while ((1 << h->bits_per) < m) ++h->bits_per;
+  h->max_batch = p->max_batch > 0 ? p->max_batch : 16;
+  halo_geometry(buffer_len, h->K, &h->left, &h->right, &h->steps_per_buf, &h->pre_first, &h->x2h);
+  h->pre_steps = h->steps_per_buf - h->pre_first;
+  h->dc = p->dc_offset;
+  h->vmin = p->v_min;
+  const double c = std::pow(10.0, (double)cspr_db / 10.0);
+  h->a_hat = (float)std::sqrt((double)p->dc_offset * c / (1.0 + c));  // reading R6
+  h->mu = p->mu;
+  h->tau = p->gate_tau < 0 ? (float)(dmin2 / 4.0) : p->gate_tau;
+  h->mode = p->update_mode;
+  int64_t tb = p->tone_bin % buffer_len;
+  if (tb < 0) tb += buffer_len;
+  h->tb_mod = (uint32_t)tb;
+  h->s32 = (uint32_t)((tb * 32) % buffer_len);
+  h->s512 = (uint32_t)((tb * 512) % buffer_len);
+  h->has_pattern = p->ref_pattern != nullptr;
+  h->P = h->has_pattern ? p->ref_len : 1;
+  h->ref_offset = p->ref_offset;
+  h->dump = p->debug_dump;
+
+  // tables in fp64, rounded once (reading R16)
+  std::vector<float2> tw(1024), tw512(512), Hs(1024), fpts(m), winit(8);
+  for (int r = 0; r < 32; ++r)
+    for (int l = 0; l < 32; ++l) {
+      const double a = -2.0 * M_PI * (double)(r * l) / 1024.0;
+      tw[r * 32 + l] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+  for (int r = 0; r < 16; ++r)
+    for (int l = 0; l < 32; ++l) {
+      const double a = -2.0 * M_PI * (double)(r * l) / 512.0;
+      tw512[r * 32 + l] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+  for (int k = 0; k < 1024; ++k) {
+    std::complex<double> acc = 0;
+    for (int t = 0; t < 203; ++t) {
+      const int i = t - 101;
+      const double a = -2.0 * M_PI * (double)(((int64_t)k * (i + 1024)) % 1024) / 1024.0;
+      acc += std::complex<double>(p->fir[2 * t], p->fir[2 * t + 1]) * std::complex<double>(std::cos(a), std::sin(a));
+    }
+    acc /= 1024.0;
+    Hs[k] = make_float2((float)acc.real(), (float)acc.imag());
+  }
+  for (int k = 0; k < m; ++k) fpts[k] = make_float2((float)pts[2 * k], (float)pts[2 * k + 1]);
+  if (p->w_init) {
+    for (int k = 0; k < 8; ++k) winit[k] = make_float2(p->w_init[2 * k], p->w_init[2 * k + 1]);
+  } else {
+    for (int k = 0; k < 8; ++k) winit[k] = make_float2(0.f, 0.f);
+    winit[1] = make_float2(1.f, 0.f);
+  }
+  std::vector<uint8_t> lab8(m);
+  for (int k = 0; k < m; ++k) lab8[k] = (uint8_t)labs[k];
+
+  auto cleanup_fail = [&](kk_status s, const std::string& msg) {
+    kk_rx_destroy(h);
+    return fail(s, msg);
+  };
+#define CKC(call)                                                                             \
+  do {                                                                                        \
+    cudaError_t _e = (call);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return cleanup_fail(_e == cudaErrorMemoryAllocation ? KK_ENOMEM : KK_ECUDA,             \
+                          std::string(#call) + ": " + cudaGetErrorString(_e));                \
+  } while (0)
+
+  if (p->cuda_stream) {
+    h->stream = (cudaStream_t)p->cuda_stream;
+  } else {
+    CKC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  CKC(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    CKC(cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&h->ev_used[i], cudaEventDisableTiming));
+  }
+  for (int i = 0; i < 4; ++i) CKC(cudaEventCreate(&h->ev_t[i]));
+  const int B = h->max_batch;
+  CKC(cudaMalloc(&h->d_tw, 1024 * sizeof(float2)));
+  CKC(cudaMalloc(&h->d_tw512, 512 * sizeof(float2)));
+  CKC(cudaMalloc(&h->d_H, 1024 * sizeof(float2)));
+  CKC(cudaMalloc(&h->d_pts, 128 * sizeof(float2)));
+  CKC(cudaMalloc(&h->d_winit, 8 * sizeof(float2)));
+  CKC(cudaMalloc(&h->d_lab, 128));
+  CKC(cudaMalloc(&h->d_pattern, (size_t)h->P));
+  CKC(cudaMalloc(&h->d_x2buf, (size_t)(h->x2h + (int64_t)B * h->N / 2) * sizeof(float2)));
+  CKC(cudaMalloc(&h->d_taps, (size_t)B * h->nsub * 8 * sizeof(float2)));
+  CKC(cudaMalloc(&h->d_counts, (size_t)B * 8 * sizeof(unsigned long long)));
+  CKC(cudaMalloc(&h->d_out, (size_t)B * h->n_sym));
+  CKC(cudaMallocHost(&h->h_counts, (size_t)B * 8 * sizeof(unsigned long long)));
+  if (h->dump & KK_DUMP_ES) CKC(cudaMalloc(&h->d_es, (size_t)B * h->N * sizeof(float2)));
+  CKC(cudaMemcpy(h->d_tw, tw.data(), 1024 * sizeof(float2), cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(h->d_tw512, tw512.data(), 512 * sizeof(float2), cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(h->d_H, Hs.data(), 1024 * sizeof(float2), cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(h->d_pts, fpts.data(), m * sizeof(float2), cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(h->d_winit, winit.data(), 8 * sizeof(float2), cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(h->d_lab, lab8.data(), m, cudaMemcpyHostToDevice));
+  if (h->has_pattern) CKC(cudaMemcpy(h->d_pattern, p->ref_pattern, (size_t)h->P, cudaMemcpyHostToDevice));
+  h->grid_x2 = x2_occupancy_grid(dev);
+  CKC(cudaGetLastError());
+#undef CKC
+  *out = h;
+  g_err.clear();
+  return KK_OK;
+}
+
+kk_status kk_rx_halo(const kk_rx_t* h, int64_t* left, int64_t* right) {
+  if (!h || !left || !right) return fail(KK_EINVAL, "bad arguments");
+  *left = h->left;
+  *right = h->right;
+  return KK_OK;
+}
+
+kk_status kk_rx_seek(kk_rx_t* h, int64_t buffer_index) {
+  if (!h) return fail(KK_EINVAL, "null handle");
+  h->stream_index = buffer_index;
+  return KK_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static kk_status run_batch(kk_rx_t* h, const int16_t* codes_dev, int nb, int64_t stream_index) {
+  const int64_t Pp = h->P;
+  int64_t n_off0 = h->has_pattern ? ((h->ref_offset + (stream_index % Pp) * (h->n_sym % Pp)) % Pp) : 0;
+  if (n_off0 < 0) n_off0 += Pp;
+  CK(cudaMemsetAsync(h->d_counts, 0, (size_t)nb * 8 * sizeof(unsigned long long), h->stream));
+  float2* x2 = h->d_x2buf + h->x2h;
+  X2Args xa{};
+  xa.codes = codes_dev;
+  xa.N = h->N;
+  xa.steps_per_buf = h->steps_per_buf;
+  xa.pre_first_step = h->pre_first;
+  xa.pre_steps = h->pre_steps;
+  xa.nbuf = nb;
+  xa.total_steps = (int64_t)h->pre_steps + (int64_t)nb * h->steps_per_buf;
+  xa.dc = h->dc;
+  xa.vmin = h->vmin;
+  xa.a_hat = h->a_hat;
+  xa.invN = (float)(1.0 / (double)h->N);
+  xa.tb_mod = h->tb_mod;
+  xa.s32 = h->s32;
+  xa.s512 = h->s512;
+  xa.x2 = x2;
+  xa.x2_lo = -h->x2h;
+  xa.tw1024 = h->d_tw;
+  xa.tw512 = h->d_tw512;
+  xa.H = h->d_H;
+  xa.counts = h->d_counts;
+  xa.es_dump = h->d_es;
+  xa.aligned16 = ((uintptr_t)codes_dev % 16) == 0;
+  if (h->timing) CK(cudaEventRecord(h->ev_t[0], h->stream));
+  CK(launch_x2(xa, h->grid_x2, h->stream));
+  if (h->timing) CK(cudaEventRecord(h->ev_t[1], h->stream));
+  LmsArgs la{};
+  la.x2 = x2;
+  la.n_sym = h->n_sym;
+  la.L = h->L;
+  la.nsub = h->nsub;
+  la.nchains = nb * h->nsub;
+  la.K = h->K;
+  la.mu = h->mu;
+  la.tau = h->tau;
+  la.mode = h->mode;
+  la.m = h->m;
+  la.pts = h->d_pts;
+  la.pattern = h->has_pattern ? h->d_pattern : nullptr;
+  la.P = Pp;
+  la.n_off0 = n_off0;
+  la.w_init = h->d_winit;
+  la.taps = h->d_taps;
+  la.counts = h->d_counts;
+  CK(launch_lms(la, h->stream));
+  if (h->timing) CK(cudaEventRecord(h->ev_t[2], h->stream));
+  ApplyArgs aa{};
+  aa.x2 = x2;
+  aa.n_sym = h->n_sym;
+  aa.L = h->L;
+  aa.nsub = h->nsub;
+  aa.total = (int64_t)nb * h->n_sym;
+  aa.m = h->m;
+  aa.pts = h->d_pts;
+  aa.labels = h->d_lab;
+  aa.pattern = h->has_pattern ? h->d_pattern : nullptr;
+  aa.P = Pp;
+  aa.n_off0 = n_off0;
+  aa.taps = h->d_taps;
+  aa.out = h->d_out;
+  aa.counts = h->d_counts;
+  CK(launch_apply(aa, h->stream));
+  if (h->timing) CK(cudaEventRecord(h->ev_t[3], h->stream));
+  h->last_launches += 3;  // kk_x2, kk_lms, kk_apply
+  return KK_OK;
+}
+
+static kk_status finish_counts(kk_rx_t* h, int nb, kk_rx_counts* out_per_buf) {
+  for (int b = 0; b < nb; ++b) {
+    const unsigned long long* c = h->h_counts + 8 * b;
+    kk_rx_counts r{};
+    r.bit_errors = c[C_BITERR];
+    r.sym_errors = c[C_SYMERR];
+    r.bits = h->has_pattern ? (uint64_t)h->n_sym * h->bits_per : 0;
+    r.symbols = (uint64_t)h->n_sym;
+    r.clipped_samples = c[C_CLIP];
+    r.gated_updates = c[C_GATED];
+    r.flags = (uint32_t)c[C_FLAGS];
+    if (out_per_buf) out_per_buf[b] = r;
+    h->totals.bit_errors += r.bit_errors;
+    h->totals.sym_errors += r.sym_errors;
+    h->totals.bits += r.bits;
+    h->totals.symbols += r.symbols;
+    h->totals.clipped_samples += r.clipped_samples;
+    h->totals.gated_updates += r.gated_updates;
+    h->totals.flags |= r.flags;
+  }
+  return KK_OK;
+}
+
+kk_status kk_rx_process_batch(kk_rx_t* h, const int16_t* first, int64_t nbuf, uint8_t* out_symbols,
+                              kk_rx_counts* out_per_buf) {
+  if (!h) return fail(KK_EINVAL, "null handle");
+  if (h->sticky != KK_OK) return fail(KK_ESTATE, "handle is in a failed state (previous CUDA error)");
+  if (!first || nbuf <= 0) return fail(KK_EINVAL, "need a buffer pointer and nbuf > 0");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  CK(cudaSetDevice(h->device));
+  struct Restore {
+    int d;
+    ~Restore() { cudaSetDevice(d); }
+  } restore{cur};
+  h->last_launches = 0;
+  const bool in_dev = is_device_ptr(first);
+  const bool out_dev = out_symbols ? is_device_ptr(out_symbols) : false;
+  const int B = h->max_batch;
+  const int64_t span_extra = h->left + h->right;
+  if (!in_dev) {
+    for (int i = 0; i < 2; ++i)
+      if (!h->d_stage[i]) {
+        cudaError_t e = cudaMalloc(&h->d_stage[i], (size_t)(span_extra + (int64_t)B * h->N) * sizeof(int16_t));
+        if (e != cudaSuccess) return fail(KK_ENOMEM, "staging allocation failed");
+      }
+  }
+  auto issue_h2d = [&](int64_t j0, int nb, int slot) -> kk_status {
+    const int16_t* src = first + j0 * h->N - h->left;
+    const size_t bytes = (size_t)(span_extra + (int64_t)nb * h->N) * sizeof(int16_t);
+    CK(cudaStreamWaitEvent(h->copy_stream, h->ev_used[slot], 0));
+    CK(cudaMemcpyAsync(h->d_stage[slot], src, bytes, cudaMemcpyHostToDevice, h->copy_stream));
+    CK(cudaEventRecord(h->ev_h2d[slot], h->copy_stream));
+    h->last_launches += 0;
+    return KK_OK;
+  };
+  int64_t j0 = 0;
+  int slot = 0;
+  if (!in_dev) {
+    kk_status s = issue_h2d(0, (int)std::min<int64_t>(B, nbuf), 0);
+    if (s != KK_OK) return s;
+  }
+  while (j0 < nbuf) {
+    const int nb = (int)std::min<int64_t>(B, nbuf - j0);
+    const int16_t* codes;
+    if (in_dev) {
+      codes = first + j0 * h->N;
+    } else {
+      CK(cudaStreamWaitEvent(h->stream, h->ev_h2d[slot], 0));
+      codes = h->d_stage[slot] + h->left;
+    }
+    kk_status s = run_batch(h, codes, nb, h->stream_index + j0);
+    if (s != KK_OK) return s;
+    if (!in_dev) {
+      CK(cudaEventRecord(h->ev_used[slot], h->stream));
+      const int64_t jn = j0 + nb;
+      if (jn < nbuf) {
+        s = issue_h2d(jn, (int)std::min<int64_t>(B, nbuf - jn), slot ^ 1);
+        if (s != KK_OK) return s;
+      }
+    }
+    if (out_symbols) {
+      CK(cudaMemcpyAsync(out_symbols + j0 * h->n_sym, h->d_out, (size_t)nb * h->n_sym,
+                         out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+    }
+    CK(cudaMemcpyAsync(h->h_counts, h->d_counts, (size_t)nb * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (h->timing) {
+      for (int k = 0; k < 3; ++k) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev_t[k], h->ev_t[k + 1]));
+        h->kernel_ms[k] += ms;
+        h->kernel_n[k] += 1;
+      }
+    }
+    finish_counts(h, nb, out_per_buf ? out_per_buf + j0 : nullptr);
+    h->last_nb = nb;
+    j0 += nb;
+    slot ^= 1;
+  }
+  h->stream_index += nbuf;
+  return KK_OK;
+}
+
+kk_status kk_rx_process(kk_rx_t* h, const int16_t* buffer, uint8_t* out_symbols, kk_rx_counts* out_errors) {
+  return kk_rx_process_batch(h, buffer, 1, out_symbols, out_errors);
+}
+
+kk_status kk_rx_get_taps(kk_rx_t* h, int64_t buf, float* out) {
+  if (!h || !out) return fail(KK_EINVAL, "bad arguments");
+  if (buf < 0 || buf >= h->last_nb) return fail(KK_EINVAL, "buffer index outside the last batch");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpy(out, h->d_taps + buf * h->nsub * 8, (size_t)h->nsub * 8 * sizeof(float2), cudaMemcpyDeviceToHost));
+  return KK_OK;
+}
+
+kk_status kk_rx_totals(const kk_rx_t* h, kk_rx_counts* out) {
+  if (!h || !out) return fail(KK_EINVAL, "bad arguments");
+  *out = h->totals;
+  return KK_OK;
+}
+
+kk_status kk_rx_reset_totals(kk_rx_t* h) {
+  if (!h) return fail(KK_EINVAL, "null handle");
+  h->totals = kk_rx_counts{};
+  return KK_OK;
+}
+
+kk_status kk_rx_debug_x2(kk_rx_t* h, int64_t first, int64_t count, float* out) {
+  if (!h || !out || count < 0) return fail(KK_EINVAL, "bad arguments");
+  if (first < -(2 * (int64_t)h->K + 2) || first + count > (int64_t)h->last_nb * h->N / 2)
+    return fail(KK_EINVAL, "x2 range outside the last batch");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpy(out, h->d_x2buf + h->x2h + first, (size_t)count * sizeof(float2), cudaMemcpyDeviceToHost));
+  return KK_OK;
+}
+
+kk_status kk_rx_debug_es(kk_rx_t* h, int64_t first, int64_t count, float* out) {
+  if (!h || !out || count < 0) return fail(KK_EINVAL, "bad arguments");
+  if (!h->d_es) return fail(KK_ESTATE, "create with debug_dump & KK_DUMP_ES");
+  if (first < 0 || first + count > (int64_t)h->last_nb * h->N) return fail(KK_EINVAL, "range outside the last batch");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpy(out, h->d_es + first, (size_t)count * sizeof(float2), cudaMemcpyDeviceToHost));
+  return KK_OK;
+}
+
+int64_t kk_rx_last_launches(const kk_rx_t* h) { return h ? h->last_launches : 0; }
+
+kk_status kk_rx_set_timing(kk_rx_t* h, int on) {
+  if (!h) return fail(KK_EINVAL, "null handle");
+  h->timing = on != 0;
+  for (int k = 0; k < 3; ++k) {
+    h->kernel_ms[k] = 0;
+    h->kernel_n[k] = 0;
+  }
+  return KK_OK;
+}
+
+kk_status kk_rx_kernel_times(const kk_rx_t* h, double* ms_out, int64_t* n_out) {
+  if (!h || !ms_out || !n_out) return fail(KK_EINVAL, "bad arguments");
+  for (int k = 0; k < 3; ++k) {
+    ms_out[k] = h->kernel_ms[k];
+    n_out[k] = h->kernel_n[k];
+  }
+  return KK_OK;
+}
+
+}  // extern "C"

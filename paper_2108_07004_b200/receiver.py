@@ -1,0 +1,187 @@
+"""Thin Python binding of the kk_rx C ABI (same names; marshalling only).
+
+Every step of the receiver runs in libkkrx.so's sm_100a kernels; this module
+only converts Python/NumPy/torch arguments into the C structs and pointers of
+include/kk_rx.h.  torch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import KKCounts, KKParams, check
+
+
+def _ptr(obj):
+    """Raw address of a torch tensor or NumPy array (no copies)."""
+    if hasattr(obj, "data_ptr"):
+        return obj.data_ptr(), obj.element_size()
+    if isinstance(obj, np.ndarray):
+        assert obj.flags["C_CONTIGUOUS"]
+        return obj.ctypes.data, obj.itemsize
+    raise TypeError(type(obj))
+
+
+def _fptr(a):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _u8ptr(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+class KKReceiver:
+    """kk_rx_create / kk_rx_process(_batch) / kk_rx_destroy."""
+
+    def __init__(self, fmt, buffer_len, cspr_db, fir, dc_offset, *, points=None, labels=None, tone_bin=541065,
+                 w_init=None, mu=1e-3, k_update=4096, sub_block=0, gate_tau=-1.0, update_mode=0, ref_pattern=None,
+                 ref_offset=0, v_min=1.0, device=-1, stream=None, debug_dump=0, max_batch=16):
+        lib = _lib.load()
+        self._lib = lib
+        p = KKParams()
+        lib.kk_rx_params_default(C.byref(p))
+        self._keep = []
+        fir = np.asarray(fir, dtype=np.complex128)
+        fir_f = np.ascontiguousarray(np.stack([fir.real, fir.imag], -1).reshape(-1).astype(np.float32))
+        self._keep.append(fir_f)
+        p.fir = _fptr(fir_f)
+        p.fir_len = len(fir)
+        p.dc_offset = float(np.float32(dc_offset))
+        p.tone_bin = int(tone_bin)
+        if w_init is not None:
+            w = np.asarray(w_init, dtype=np.complex128).reshape(8)
+            wf = np.ascontiguousarray(np.stack([w.real, w.imag], -1).reshape(-1).astype(np.float32))
+            self._keep.append(wf)
+            p.w_init = _fptr(wf)
+        p.mu = mu
+        p.k_update = k_update
+        p.sub_block = sub_block
+        p.gate_tau = gate_tau
+        p.update_mode = update_mode
+        if points is not None:
+            pts = np.asarray(points, dtype=np.complex128)
+            pf = np.ascontiguousarray(np.stack([pts.real, pts.imag], -1).reshape(-1).astype(np.float32))
+            lb = np.ascontiguousarray(np.asarray(labels, dtype=np.uint8))
+            self._keep += [pf, lb]
+            p.points = _fptr(pf)
+            p.labels = _u8ptr(lb)
+            p.m = len(pts)
+        if ref_pattern is not None:
+            rp = np.ascontiguousarray(np.asarray(ref_pattern, dtype=np.uint8))
+            self._keep.append(rp)
+            p.ref_pattern = _u8ptr(rp)
+            p.ref_len = len(rp)
+        p.ref_offset = int(ref_offset)
+        p.v_min = v_min
+        p.device = device
+        p.cuda_stream = stream
+        p.debug_dump = debug_dump
+        p.max_batch = max_batch
+        fmt_id = _lib.FORMATS[fmt] if isinstance(fmt, str) else int(fmt)
+        h = C.c_void_p()
+        check(lib.kk_rx_create(C.byref(h), fmt_id, 4, int(buffer_len), float(cspr_db), C.byref(p)), "kk_rx_create")
+        self.h = h
+        self.buffer_len = int(buffer_len)
+        self.n_sym = self.buffer_len // 4
+        self.nsub = self.n_sym // (sub_block if sub_block > 0 else self.n_sym)
+        self.max_batch = max_batch
+
+    # ------------------------------------------------------------------
+    def halo(self):
+        l, r = C.c_int64(), C.c_int64()
+        check(self._lib.kk_rx_halo(self.h, C.byref(l), C.byref(r)), "kk_rx_halo")
+        return l.value, r.value
+
+    def seek(self, buffer_index):
+        check(self._lib.kk_rx_seek(self.h, int(buffer_index)), "kk_rx_seek")
+
+    def process_batch(self, stream, offset, nbuf, out=None):
+        """stream: int16 torch tensor (cuda or pinned cpu) or NumPy array holding
+        the contiguous sample stream; offset: index of buffer 0's first sample.
+        out: uint8 tensor/array of nbuf*N/4 labels or None.  Returns a list of
+        per-buffer counter dicts."""
+        base, es = _ptr(stream)
+        assert es == 2
+        optr = None
+        if out is not None:
+            optr, _ = _ptr(out)
+        cnt = (KKCounts * int(nbuf))()
+        check(self._lib.kk_rx_process_batch(self.h, C.c_void_p(base + 2 * int(offset)), int(nbuf),
+                                            C.c_void_p(optr) if optr is not None else None, cnt),
+              "kk_rx_process_batch")
+        return [c.as_dict() for c in cnt]
+
+    def process(self, stream, offset, out=None):
+        return self.process_batch(stream, offset, 1, out)[0]
+
+    def taps(self, buf=0):
+        a = np.empty(self.nsub * 16, dtype=np.float32)
+        check(self._lib.kk_rx_get_taps(self.h, int(buf), _fptr(a)), "kk_rx_get_taps")
+        c = a.reshape(self.nsub, 8, 2)
+        return c[..., 0] + 1j * c[..., 1]
+
+    def totals(self):
+        c = KKCounts()
+        check(self._lib.kk_rx_totals(self.h, C.byref(c)), "kk_rx_totals")
+        return c.as_dict()
+
+    def reset_totals(self):
+        check(self._lib.kk_rx_reset_totals(self.h), "kk_rx_reset_totals")
+
+    def debug_x2(self, first, count):
+        a = np.empty(2 * count, dtype=np.float32)
+        check(self._lib.kk_rx_debug_x2(self.h, int(first), int(count), _fptr(a)), "kk_rx_debug_x2")
+        return a[0::2] + 1j * a[1::2].astype(np.float64)
+
+    def debug_es(self, first, count):
+        a = np.empty(2 * count, dtype=np.float32)
+        check(self._lib.kk_rx_debug_es(self.h, int(first), int(count), _fptr(a)), "kk_rx_debug_es")
+        return a[0::2] + 1j * a[1::2].astype(np.float64)
+
+    def last_launches(self):
+        return int(self._lib.kk_rx_last_launches(self.h))
+
+    def set_timing(self, on=True):
+        check(self._lib.kk_rx_set_timing(self.h, 1 if on else 0), "kk_rx_set_timing")
+
+    def kernel_times(self):
+        ms = (C.c_double * 3)()
+        n = (C.c_int64 * 3)()
+        check(self._lib.kk_rx_kernel_times(self.h, ms, n), "kk_rx_kernel_times")
+        return {k: (ms[i], n[i]) for i, k in enumerate(("kk_x2", "kk_lms", "kk_apply"))}
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.kk_rx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def builtin_constellation(fmt):
+    lib = _lib.load()
+    pts = np.empty(256, dtype=np.float32)
+    lab = np.empty(128, dtype=np.uint8)
+    m = lib.kk_rx_constellation(_lib.FORMATS[fmt], _fptr(pts), _u8ptr(lab))
+    if m < 0:
+        raise ValueError(fmt)
+    return pts[0:2 * m:2] + 1j * pts[1:2 * m:2].astype(np.float64), lab[:m].astype(np.int64)
+
+
+def halo_for(buffer_len, k_update=4096):
+    lib = _lib.load()
+    l, r = C.c_int64(), C.c_int64()
+    check(lib.kk_rx_halo_for(int(buffer_len), int(k_update), C.byref(l), C.byref(r)), "kk_rx_halo_for")
+    return l.value, r.value

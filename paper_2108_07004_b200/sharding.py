@@ -1,0 +1,59 @@
+"""Multi-GPU plumbing: buffer sharding and counter reduction.
+
+The KK chain shards buffer-by-buffer: the outputs of buffer b depend only on the
+raw window [bN - left, (b+1)N + right) (adaptive taps restart per sub-block,
+reading R10; the tone phase is buffer-local, reading R7), so ranks process
+disjoint buffer ranges with no data-path collective.  The only collective is
+one all_reduce(SUM) of the int64 error counters (and MAX of elapsed time) at
+the end of a run or report window -- torch.distributed over NCCL on B200s,
+gloo in the CPU tests.
+"""
+from __future__ import annotations
+
+COUNT_KEYS = ("bit_errors", "sym_errors", "bits", "symbols", "clipped_samples", "gated_updates")
+
+
+def shard_range(n_buffers: int, world: int, rank: int):
+    """Contiguous buffer range [lo, hi) of `rank` (sizes differ by at most 1)."""
+    if world <= 0 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    base, extra = divmod(int(n_buffers), int(world))
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def weak_step_buffers(step: int, rank: int, world: int, batch: int, pool: int):
+    """First pool buffer of `rank`'s batch in `step` for a weak-scaling run that
+    cycles a pool of distinct buffers (each rank a different batch per step)."""
+    return (rank * batch + step * batch * world) % pool
+
+
+def sum_counts(per_buffer):
+    tot = {k: 0 for k in COUNT_KEYS}
+    flags = 0
+    for c in per_buffer:
+        for k in COUNT_KEYS:
+            tot[k] += int(c[k])
+        flags |= int(c.get("flags", 0))
+    tot["flags"] = flags
+    return tot
+
+
+def reduce_counts(local: dict, elapsed_ms: float, device=None, group=None):
+    """all_reduce(SUM) of the counters and all_reduce(MAX) of the elapsed time."""
+    import torch
+    import torch.distributed as dist
+
+    v = torch.tensor([int(local[k]) for k in COUNT_KEYS] + [int(local.get("flags", 0))], dtype=torch.int64,
+                     device=device)
+    t = torch.tensor([float(elapsed_ms)], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized():
+        flags = v[-1:].clone()
+        dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+        v[-1] = flags[0]
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    out = {k: int(v[i]) for i, k in enumerate(COUNT_KEYS)}
+    out["flags"] = int(v[-1])
+    return out, float(t.item())

@@ -1,0 +1,71 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the sharding / reduction
+logic used by bench.py under torchrun.  The GPU data path has no collective;
+these cover the host-side plumbing."""
+import os
+import socket
+
+import pytest
+
+from paper_2108_07004_b200.sharding import shard_range, sum_counts, weak_step_buffers
+
+
+def test_shard_range_partitions():
+    for n in (1, 7, 16, 4096):
+        for w in (1, 2, 3, 8):
+            got = []
+            for r in range(w):
+                lo, hi = shard_range(n, w, r)
+                got += list(range(lo, hi))
+            assert got == list(range(n))
+
+
+def test_weak_steps_disjoint_within_step():
+    for w in (1, 2, 4, 8):
+        firsts = {weak_step_buffers(3, r, w, 16, 64 * 16) for r in range(w)}
+        assert len(firsts) == w
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2108_07004_b200.sharding import reduce_counts
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard_range(10, world, rank)
+    # fake per-buffer counters: buffer b has b bit errors, flags only on buffer 7
+    per = [dict(bit_errors=b, sym_errors=b // 2, bits=100, symbols=25, clipped_samples=0, gated_updates=1,
+                flags=1 if b == 7 else 0) for b in range(lo, hi)]
+    tot, tmax = reduce_counts(sum_counts(per), 10.0 + rank)
+    q.put((rank, tot, tmax))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_reduction():
+    torch = pytest.importorskip("torch")
+    import torch.multiprocessing as tmp
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, tot, tmax in res:
+        assert tot["bit_errors"] == sum(range(10))
+        assert tot["sym_errors"] == sum(b // 2 for b in range(10))
+        assert tot["bits"] == 1000 and tot["symbols"] == 250
+        assert tot["flags"] == 1
+        assert tmax == 11.0
+    assert torch is not None

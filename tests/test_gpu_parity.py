@@ -1,0 +1,236 @@
+"""GPU parity of libkkrx.so (through the C ABI) against the float64 oracle.
+
+Contract (BASELINE.json north_star):
+  * E_s (S3 output) rel-L2 <= 1e-5 per buffer (fp32 vs fp64)
+  * x2 (S4 output) rel-L2 <= 1e-5
+  * adaptive taps: max |dw| <= 1e-4 (soft gate is Lipschitz; reading R10)
+  * decisions identical for every symbol whose oracle Voronoi margin >= 1e-4
+  * GPU counters == host recount of the GPU's own decisions, exactly
+  * counts on non-exempt symbols == oracle, exactly; totals bit-identical when
+    the exempt set is empty
+"""
+import numpy as np
+import pytest
+
+from oracle import kk_oracle as O
+from synth import configs
+from synth.generate import LinkConfig, make_pool, make_stream
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+EXEMPT = 1e-4
+TOL_FIELD = 1e-5
+TOL_TAPS = 1e-4
+
+
+def _fir(name):
+    h = np.loadtxt(f"data/fir/{name}.txt")
+    return h[:, 0] + 1j * h[:, 1]
+
+
+def _require_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _gpu_run(pool, cfg, fir, nbuf, first=0, dump=True, max_batch=None, host_input=False, **kw):
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    left, right = halo_for(cfg.buffer_len, kw.get("k_update", 4096))
+    stream, off = make_stream(pool, nbuf, left, right, first=first)
+    rx = KKReceiver(cfg.fmt if cfg.fmt.startswith("QAM") else "CUSTOM", cfg.buffer_len, cfg.cspr_db, fir,
+                    pool.dc_offset, points=pool.points, labels=pool.labels, tone_bin=cfg.tbin,
+                    ref_pattern=pool.pattern, debug_dump=1 if dump else 0, max_batch=max_batch or nbuf, **kw)
+    n_sym = cfg.buffer_len // 4
+    if host_input:
+        src = torch.from_numpy(stream).pin_memory()
+        out = torch.empty(nbuf * n_sym, dtype=torch.uint8).pin_memory()
+    else:
+        src = torch.from_numpy(stream).cuda()
+        out = torch.empty(nbuf * n_sym, dtype=torch.uint8, device="cuda")
+    rx.seek(first)
+    counts = rx.process_batch(src, off, nbuf, out)
+    res = dict(counts=counts, labels=out.cpu().numpy(), stream=stream, off=off, left=left, right=right, rx=rx)
+    return res
+
+
+def _oracle(stream, off, b, cfg, pool, fir, left, right, **kw):
+    n = cfg.buffer_len
+    win = stream[off + b * n - left: off + (b + 1) * n + right]
+    p = O.RxParams(buffer_len=n, cspr_db=cfg.cspr_db, dc_offset=pool.dc_offset, fir=fir, points=pool.points,
+                   labels=pool.labels, tone_bin=cfg.tbin, pattern=pool.pattern, **kw)
+    return O.receive(win, left, p, want_stages=True)
+
+
+def _check_buffer(g, o, b, cfg, pool, check_es=True):
+    rx = g["rx"]
+    n = cfg.buffer_len
+    n_sym = n // 4
+    report = {}
+    if check_es:
+        es_g = rx.debug_es(b * n, n)
+        es_o = o["e_s"][0 - o["e_pos0"]: n - o["e_pos0"]]
+        report["es_rel"] = np.linalg.norm(es_g - es_o) / np.linalg.norm(es_o)
+        assert report["es_rel"] <= TOL_FIELD, report
+    x2_first = o["x2_first"]
+    x2_o = o["x2"]
+    x2_g = rx.debug_x2(b * n // 2 + x2_first, len(x2_o))
+    report["x2_rel"] = np.linalg.norm(x2_g - x2_o) / np.linalg.norm(x2_o)
+    assert report["x2_rel"] <= TOL_FIELD, report
+    taps_g = rx.taps(b)
+    for q, (w, gg) in enumerate(o["taps"]):
+        d = np.max(np.abs(taps_g[q] - np.r_[w, gg]))
+        report["taps_dmax"] = max(report.get("taps_dmax", 0.0), d)
+    assert report["taps_dmax"] <= TOL_TAPS, report
+    # decisions
+    inv = np.argsort(pool.labels)
+    lab_g = g["labels"][b * n_sym:(b + 1) * n_sym].astype(np.int64)
+    dec_g = inv[lab_g]
+    ok = o["margin"] >= EXEMPT
+    report["exempt"] = int((~ok).sum())
+    mism = np.nonzero((dec_g != o["decisions"]) & ok)[0]
+    assert mism.size == 0, (report, mism[:10])
+    # GPU counters == recount of GPU decisions
+    c = g["counts"][b]
+    ref = o["ref"]
+    re_ = O.count_errors(dec_g, ref, pool.labels)
+    assert c["sym_errors"] == re_["sym_errors"] and c["bit_errors"] == re_["bit_errors"], (c, re_)
+    assert c["symbols"] == n_sym and c["bits"] == re_["bits"]
+    # non-exempt counts == oracle
+    ro = O.count_errors(o["decisions"][ok], ref[ok], pool.labels)
+    rg = O.count_errors(dec_g[ok], ref[ok], pool.labels)
+    assert ro == rg
+    if report["exempt"] == 0:
+        assert c["sym_errors"] == o["sym_errors"] and c["bit_errors"] == o["bit_errors"]
+    assert c["clipped_samples"] == o["clipped"]
+    assert c["gated_updates"] <= o["gated_updates"] + 8 and c["gated_updates"] >= o["gated_updates"] - 8
+    return report
+
+
+@pytest.mark.parametrize("name,nbuf", [("C1_n16", 2), ("C2_n16", 3), ("C4_n16", 2), ("C5_n16", 2),
+                                       ("C3_GS8_c8_o10_n16", 2), ("C3_QAM32_c14_o22_n16", 2)])
+def test_parity_small(name, nbuf):
+    _require_gpu()
+    wl = configs.get(name)
+    cfg = wl.link
+    pool = make_pool(cfg, max(nbuf, 2))
+    fir = _fir(name)
+    g = _gpu_run(pool, cfg, fir, nbuf)
+    for b in range(nbuf):
+        o = _oracle(g["stream"], g["off"], b, cfg, pool, fir, g["left"], g["right"])
+        rep = _check_buffer(g, o, b, cfg, pool)
+        print(name, b, rep)
+
+
+def test_parity_ragged_buffer_len():
+    """buffer_len = 129*512 (not a multiple of the 3072-sample step: ragged tail)."""
+    _require_gpu()
+    cfg = LinkConfig("QAM16", 14.0, 20.0, "one_sided", 129 * 512, seed_noise=55)
+    pool = make_pool(cfg, 2)
+    fir = _fir("C2_n16")
+    g = _gpu_run(pool, cfg, fir, 2)
+    for b in range(2):
+        o = _oracle(g["stream"], g["off"], b, cfg, pool, fir, g["left"], g["right"])
+        _check_buffer(g, o, b, cfg, pool)
+
+
+@pytest.mark.parametrize("kw", [dict(update_mode=1), dict(sub_block=2048), dict(k_update=1000, mu=2e-3),
+                                dict(update_mode=0, gate_tau=0.0)])
+def test_parity_update_variants(kw):
+    """PILOT mode (paper's training mode), sub-blocks L < N/4 (chains inside the
+    buffer), other K / mu, and hard gate (tau = 0; compared stage-wise)."""
+    _require_gpu()
+    name = "C2_n16"
+    wl = configs.get(name)
+    cfg = wl.link
+    pool = make_pool(cfg, 2)
+    fir = _fir(name)
+    g = _gpu_run(pool, cfg, fir, 2, **kw)
+    okw = {}
+    if "update_mode" in kw:
+        okw["update_mode"] = kw["update_mode"]
+    if "sub_block" in kw:
+        okw["sub_block"] = kw["sub_block"]
+    if "k_update" in kw:
+        okw["k_update"] = kw["k_update"]
+    if "mu" in kw:
+        okw["mu"] = kw["mu"]
+    if "gate_tau" in kw:
+        okw["gate_tau"] = kw["gate_tau"]
+    for b in range(2):
+        o = _oracle(g["stream"], g["off"], b, cfg, pool, fir, g["left"], g["right"], **okw)
+        if kw.get("gate_tau") == 0.0:
+            # hard DD: x2 parity only (the trajectory is not Lipschitz)
+            x2_g = g["rx"].debug_x2(b * cfg.buffer_len // 2 + o["x2_first"], len(o["x2"]))
+            assert np.linalg.norm(x2_g - o["x2"]) / np.linalg.norm(o["x2"]) <= TOL_FIELD
+        else:
+            _check_buffer(g, o, b, cfg, pool, check_es=False)
+
+
+def test_sharding_and_memory_kind_invariance():
+    """Outputs depend only on the raw window: a 4-buffer batch, 4 single-buffer
+    calls (max_batch=1), and host (pinned) input give bit-identical labels,
+    counters and taps (SURVEY 8(b) determinism; multi-GPU sharding relies on it)."""
+    _require_gpu()
+    name = "C2_n16"
+    wl = configs.get(name)
+    cfg = wl.link
+    pool = make_pool(cfg, 4)
+    fir = _fir(name)
+    a = _gpu_run(pool, cfg, fir, 4, dump=False)
+    b = _gpu_run(pool, cfg, fir, 4, dump=False, max_batch=1)
+    c = _gpu_run(pool, cfg, fir, 4, dump=False, max_batch=3, host_input=True)
+    assert np.array_equal(a["labels"], b["labels"]) and np.array_equal(a["labels"], c["labels"])
+    assert a["counts"] == b["counts"] == c["counts"]
+    assert np.array_equal(a["rx"].taps(3), b["rx"].taps(0))
+    # one buffer at stream position 2 alone == buffer 2 of the batch
+    d = _gpu_run(pool, cfg, fir, 1, first=2, dump=False)
+    n_sym = cfg.buffer_len // 4
+    assert np.array_equal(d["labels"], a["labels"][2 * n_sym:3 * n_sym])
+    assert d["counts"][0] == a["counts"][2]
+
+
+def test_full_size_c1_noiseless():
+    """C1 at the paper's buffer size (2^22 samples, 2^20 symbols): E_s and x2
+    parity over the whole buffer; zero errors, bit-identical totals."""
+    _require_gpu()
+    name = "C1"
+    wl = configs.get(name)
+    cfg = wl.link
+    pool = make_pool(cfg, 1)
+    fir = _fir(name)
+    g = _gpu_run(pool, cfg, fir, 1)
+    o = _oracle(g["stream"], g["off"], 0, cfg, pool, fir, g["left"], g["right"])
+    rep = _check_buffer(g, o, 0, cfg, pool)
+    assert rep["exempt"] == 0
+    assert g["counts"][0]["sym_errors"] == 0 and g["counts"][0]["bit_errors"] == 0 == o["bit_errors"]
+
+
+def test_full_size_c5_bench_launch_config():
+    """C5 (GS-128, the bench workload) at full size in the bench's launch
+    configuration (device-resident, max_batch 16): one buffer of a 3-buffer
+    batch checked against the oracle."""
+    _require_gpu()
+    name = "C5"
+    wl = configs.get(name)
+    cfg = wl.link
+    pool = make_pool(cfg, 3)
+    fir = _fir(name)
+    g = _gpu_run(pool, cfg, fir, 3, max_batch=16)
+    o = _oracle(g["stream"], g["off"], 1, cfg, pool, fir, g["left"], g["right"])
+    rep = _check_buffer(g, o, 1, cfg, pool)
+    print("C5 full", rep)
+
+
+def test_empty_and_invalid_calls():
+    _require_gpu()
+    from paper_2108_07004_b200._lib import KKError
+    wl = configs.get("C1_n16")
+    cfg = wl.link
+    pool = make_pool(cfg, 1)
+    g = _gpu_run(pool, cfg, _fir("C1_n16"), 1, dump=False)
+    with pytest.raises(KKError):
+        g["rx"].process_batch(torch.from_numpy(g["stream"]).cuda(), g["off"], 0)
+    with pytest.raises(KKError):
+        g["rx"].taps(5)
