@@ -36,7 +36,8 @@ METRIC = "sustained GSa/s (equiv. GBaud) on full KK chain, 1/2/4/8 B200; % HBM r
 UNIT = "GSa/s"
 # algorithmic work per ADC sample
 HBM_BYTES_PER_SA = 2.25          # int16 in + uint8 label per 4 samples out
-FLOP_PER_SA_X2 = 217.0           # kk_x2: Hilbert 100 + static EQ 97 + pointwise S1/S3 20
+FLOP_PER_SA_KERNEL = 238.0       # kk_chain_kernel<APPLY>: Hilbert 100 + static EQ 97 + pointwise S1/S3 20
+                                 # + WL apply 16 + decision ~5 (everything but the update pass)
 FLOP_PER_SA_CHAIN = 240.0        # whole chain (+ WL apply 16, decision ~5, update ~0.2)
 # FP32 SIMT peak derived from the unit counts and max clock (B200_PROFILING.md):
 # 148 SMs x 128 FP32 lanes x 2 flop (FFMA) x 1.965 GHz
@@ -308,14 +309,13 @@ def run_gpu(args):
 
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    x2_ms, x2_n = ktimes["kk_x2"]
-    x2_avg_ms = x2_ms / max(x2_n, 1)
-    x2_flops = FLOP_PER_SA_X2 * B * N
-    achieved_tf = x2_flops / (x2_avg_ms / 1e3) / 1e12
+    ch_ms, ch_n = ktimes["chain"]
+    ch_avg_ms = ch_ms / max(ch_n, 1)
+    achieved_tf = FLOP_PER_SA_KERNEL * B * N / (ch_avg_ms / 1e3) / 1e12
     traffic = profile_traffic()
     step_ms = ms_max / args.steps
-    lms_avg = ktimes["kk_lms"][0] / max(ktimes["kk_lms"][1], 1)
-    app_avg = ktimes["kk_apply"][0] / max(ktimes["kk_apply"][1], 1)
+    tail_avg = ktimes["x2_pass"][0] / max(ktimes["x2_pass"][1], 1)
+    lms_avg = ktimes["lms"][0] / max(ktimes["lms"][1], 1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -329,12 +329,14 @@ def run_gpu(args):
         "gbaud_equiv": value / 4.0,
         "hbm_fraction": value * HBM_BYTES_PER_SA / hbm,
         "fp32_fraction_chain": value * FLOP_PER_SA_CHAIN / (FP32_PEAK_TFLOPS * 1e3),
-        "roofline": {"bound": "alu", "kernel": "kk_x2", "achieved": achieved_tf, "peak": FP32_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved_tf / FP32_PEAK_TFLOPS,
-                     "traffic": (traffic or {}).get("kk_x2_bytes_per_launch_scaled", None) if traffic else None,
-                     "flop_per_sa": FLOP_PER_SA_X2, "avg_launch_ms": x2_avg_ms,
+        "roofline": {"bound": "alu", "kernel": "kk_chain_kernel<APPLY>", "achieved": achieved_tf,
+                     "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tf / FP32_PEAK_TFLOPS,
+                     "traffic": (traffic or {}).get("chain_dram_bytes_per_launch") if traffic else None,
+                     "flop_per_sa": FLOP_PER_SA_KERNEL, "samples_per_launch": B * N, "avg_launch_ms": ch_avg_ms,
+                     "hbm_algorithmic_bytes_per_launch": HBM_BYTES_PER_SA * B * N,
+                     "hbm_achieved_gbs": HBM_BYTES_PER_SA * B * N / (ch_avg_ms / 1e3) / 1e9,
                      "peak_basis": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (derived, DESIGN.md)"},
-        "kernel_ms_per_step": {"kk_x2": x2_avg_ms, "kk_lms": lms_avg, "kk_apply": app_avg},
+        "kernel_ms_per_step": {"x2_tails": tail_avg, "lms": lms_avg, "chain": ch_avg_ms},
         "errors": {"bit_errors": int(agg[0]), "bits": int(agg[1]), "ber": int(agg[0]) / max(int(agg[1]), 1)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -360,7 +362,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kk", choices=["kk", "reference"])
     ap.add_argument("--workload", default="C5")
-    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--pool", type=int, default=16)
     ap.add_argument("--ref-workers", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")

@@ -62,6 +62,8 @@ typedef enum {
 typedef enum { KK_UPD_DD_SOFT = 0, KK_UPD_PILOT = 1, KK_UPD_DD_HARD = 2 } kk_update_mode;
 
 #define KK_DUMP_ES 1u /* keep E_s (after S3) of the last call for kk_rx_debug_es() */
+#define KK_DUMP_X2 2u /* materialise x2 (after S4) of the whole last batch for kk_rx_debug_x2()
+                       * (by default only the update-pass tails are materialised) */
 
 typedef struct {
   float dc_offset;          /* d, ADC-code units, added before sqrt/log */
@@ -150,7 +152,9 @@ kk_status kk_rx_reset_totals(kk_rx_t *h);
 
 /* Debug (parity tests): x2 (S4 output, 2 sps) of the last internal batch,
  * x2 index relative to that batch's first buffer (x2 index m <-> 4-sps position
- * 2m); valid range [-(2*k_update+2), nbuf*buffer_len/2).  2*count floats. */
+ * 2m); valid range [-(2*k_update+2), nbuf*buffer_len/2) with KK_DUMP_X2 (or
+ * sub_block < buffer_len/4); otherwise only the update-pass tails
+ * [b*N/2 - 2*k_update - 2, b*N/2) are defined.  2*count floats. */
 kk_status kk_rx_debug_x2(kk_rx_t *h, int64_t first, int64_t count, float *out);
 
 /* Debug: E_s (S3 output, 4 sps) of the last internal batch (needs
@@ -166,7 +170,9 @@ int64_t kk_rx_last_launches(const kk_rx_t *h);
 /* Per-kernel device timing (CUDA events recorded on the launch stream around
  * each kernel of every internal batch).  kk_rx_set_timing(h, 1) enables and
  * resets; kk_rx_kernel_times returns accumulated milliseconds and launch
- * counts for {kk_x2, kk_lms, kk_apply} (3 entries each). */
+ * counts of 3 slots: [0] S1-S4 x2 pass (update-pass tails, or the whole batch
+ * when sub_block < buffer), [1] the LMS update pass, [2] the fused
+ * S1-S7 chain kernel (or the apply kernel when sub_block < buffer). */
 kk_status kk_rx_set_timing(kk_rx_t *h, int on);
 kk_status kk_rx_kernel_times(const kk_rx_t *h, double *ms_out, int64_t *n_out);
 

@@ -7,15 +7,25 @@
 // four-step factorisation 1024 = 32 x 32:
 //   pass A: 32-point DFT over the register index (in registers, no memory)
 //   twiddle W_1024^(lane*r) from a 32x32 shared table
-//   one 32x32 transpose through a per-warp padded shared tile
+//   one 32x32 transpose through a per-warp padded shared tile (re, then im)
 //   pass B: 32-point DFT over the register index
 // so each point crosses shared memory once per transform (not once per radix-2
-// stage as a shared-memory Stockham would), and all butterflies are FP32
-// FFMA/FADD with compile-time twiddles (immediate operands).
+// stage as a shared-memory Stockham would).
+//
+// The 32-point DFT is radix-2 decimation in TIME with the twiddle folded into
+// the butterfly as FFMAs: for w = c(1 + i t) (t = tan),
+//   p = b.x - t b.y, q = b.y + t b.x;  a +- w b = (a.x +- c p, a.y +- c q)
+// = 6 FP32 instructions per general butterfly (8 for mul-then-add), 4 for
+// trivial twiddles; all twiddle constants are immediates.
+//
+// Code size matters (an early version with every transform inlined at five
+// call sites was instruction-fetch bound, 271 KB of SASS): there is exactly ONE
+// copy of the 32-point and of the 16-point DFT; passes and transforms are loops
+// (#pragma unroll 1) around them, and every inverse transform is computed as
+// conj(DFT(conj(x))).
 //
 // Layout contract ("lane layout"): element e of a length-1024 sequence lives in
-// lane (e % 32), register (e / 32).  Forward and inverse transforms both take
-// and return this layout, so FFT -> pointwise -> IFFT needs no reordering.
+// lane (e % 32), register (e / 32), for inputs and outputs alike.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -44,113 +54,158 @@ __device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2
 __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
-__device__ __forceinline__ float2 c_mulc(float2 a, float2 b) {  // a * conj(b)
-  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
-}
+__device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
 
-// a * exp(S*2*pi*i*m/32), m a compile-time constant after unrolling; S = -1 forward, +1 inverse.
-template <int S>
+// a * exp(-2*pi*i*m/32) (used outside the butterflies)
 __device__ __forceinline__ float2 tw32(float2 a, int m) {
   m &= 31;
   if (m == 0) return a;
   if (m == 16) return make_float2(-a.x, -a.y);
-  if (m == 8) return (S > 0) ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);    // *(+-i)
-  if (m == 24) return (S > 0) ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+  if (m == 8) return make_float2(a.y, -a.x);
+  if (m == 24) return make_float2(-a.y, a.x);
   const float c = cos32(m);
-  const float s = (S > 0) ? sin32(m) : -sin32(m);
-  if (m == 4 || m == 12 || m == 20 || m == 28) {
-    // |c| == |s| == sqrt(1/2): (a.x c - a.y s, a.x s + a.y c) with one multiply each
-    return make_float2((a.x * (c > 0 ? 1.f : -1.f) - a.y * (s > 0 ? 1.f : -1.f)) * 0.70710678118654752f,
-                       (a.x * (s > 0 ? 1.f : -1.f) + a.y * (c > 0 ? 1.f : -1.f)) * 0.70710678118654752f);
-  }
+  const float s = -sin32(m);
   return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
 }
 
-// In-register radix-2 decimation-in-frequency DFT of length N (N | 32) over v[0..N):
-//   V[k] = sum_n v[n] exp(S*2*pi*i*n*k/N),  result V[k] stored at v[brev(k)].
-template <int N, int S>
-__device__ __forceinline__ void dft_dif(float2 (&v)[N]) {
-  constexpr int LOGN = (N == 2) ? 1 : (N == 4) ? 2 : (N == 8) ? 3 : (N == 16) ? 4 : 5;
-#pragma unroll
-  for (int st = 0; st < LOGN; ++st) {
-    const int span = N >> (st + 1);
-#pragma unroll
-    for (int start = 0; start < N; start += 2 * span) {
-#pragma unroll
-      for (int j = 0; j < span; ++j) {
-        float2 a = v[start + j], b = v[start + j + span];
-        v[start + j] = c_add(a, b);
-        // twiddle W_{2 span}^j = W_32^{j * 32 / (2 span)}
-        v[start + j + span] = tw32<S>(c_sub(a, b), j * (32 / (2 * span)));
-      }
+// DIT butterfly: (a, b) <- (a + w b, a - w b), w = exp(-2 pi i m / 32), m compile-time.
+__device__ __forceinline__ void bfly(float2& a, float2& b, int m) {
+  m &= 31;
+  if (m == 0) {
+    const float2 t = b;
+    b = c_sub(a, t);
+    a = c_add(a, t);
+  } else if (m == 8) {  // w = -i: w b = (b.y, -b.x)
+    const float2 t = make_float2(b.y, -b.x);
+    b = c_sub(a, t);
+    a = c_add(a, t);
+  } else if (m == 24) {  // w = +i
+    const float2 t = make_float2(-b.y, b.x);
+    b = c_sub(a, t);
+    a = c_add(a, t);
+  } else if (m == 16) {
+    const float2 t = make_float2(-b.x, -b.y);
+    b = c_sub(a, t);
+    a = c_add(a, t);
+  } else {
+    // w = c (1 + i t) with c = cos, t = tan (|t| <= tan(3 pi / 8) for the angles used)
+    const float c = cos32(m);
+    const float s = -sin32(m);
+    if (m == 4 || m == 12 || m == 20 || m == 28) {
+      // |t| == 1: p = b.x - t b.y, q = b.y + t b.x are plain adds
+      const float t = s / c;
+      const float p = (t > 0) ? b.x - b.y : b.x + b.y;
+      const float q = (t > 0) ? b.y + b.x : b.y - b.x;
+      const float2 a0 = a;
+      a = make_float2(fmaf(c, p, a0.x), fmaf(c, q, a0.y));
+      b = make_float2(fmaf(-c, p, a0.x), fmaf(-c, q, a0.y));
+    } else if (m < 4 || (m > 12 && m < 20) || m > 28) {
+      // |cos| > |sin|: factor cos
+      const float t = s / c;
+      const float p = fmaf(-t, b.y, b.x), q = fmaf(t, b.x, b.y);
+      const float2 a0 = a;
+      a = make_float2(fmaf(c, p, a0.x), fmaf(c, q, a0.y));
+      b = make_float2(fmaf(-c, p, a0.x), fmaf(-c, q, a0.y));
+    } else {
+      // |sin| > |cos|: w = s (ct + i) with ct = c/s:  w b = s (ct b.x - b.y, ct b.y + b.x)
+      const float ct = c / s;
+      const float p = fmaf(ct, b.x, -b.y), q = fmaf(ct, b.y, b.x);
+      const float2 a0 = a;
+      a = make_float2(fmaf(s, p, a0.x), fmaf(s, q, a0.y));
+      b = make_float2(fmaf(-s, p, a0.x), fmaf(-s, q, a0.y));
     }
   }
 }
 
-// Natural-order DFT over the register index: v[k] = sum_n v_in[n] W_N^{S n k}.
-template <int N, int S>
+// Forward DFT of length N (N in {16, 32}) over the register index, natural order:
+//   v[k] <- sum_n v[n] exp(-2 pi i n k / N)
+// radix-2 decimation in time; the input bit-reversal is a compile-time renaming.
+template <int N>
 __device__ __forceinline__ void dft_reg(float2 (&v)[N]) {
-  dft_dif<N, S>(v);
+  constexpr int LOGN = (N == 16) ? 4 : 5;
   float2 t[N];
 #pragma unroll
-  for (int k = 0; k < N; ++k) t[k] = v[brev(k, (N == 16) ? 4 : 5)];
+  for (int k = 0; k < N; ++k) t[k] = v[brev(k, LOGN)];
+#pragma unroll
+  for (int st = 0; st < LOGN; ++st) {
+    const int half = 1 << st;  // butterfly span
+#pragma unroll
+    for (int start = 0; start < N; start += 2 * half) {
+#pragma unroll
+      for (int j = 0; j < half; ++j) bfly(t[start + j], t[start + j + half], j * (32 / (2 * half)));
+    }
+  }
 #pragma unroll
   for (int k = 0; k < N; ++k) v[k] = t[k];
 }
 
-// 1024-point DFT of one warp, lane layout in and out.
-//   S = -1: X[k] = sum_n x[n] e^{-2 pi i n k / 1024}
-//   S = +1: x[n] = sum_k X[k] e^{+2 pi i n k / 1024}   (unnormalised)
-// scr: this warp's 32 x 33 float2 tile; tw: shared table tw[r*32 + l] = e^{-2 pi i r l / 1024}.
-template <int S>
-__device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float2* __restrict__ scr,
+// Forward 1024-point DFT of one warp, lane layout in and out:
+//   X[k] = sum_n x[n] e^{-2 pi i n k / 1024}
+// scr: this warp's 32 x 33 float tile; tw: shared table tw[r*32 + l] = e^{-2 pi i r l / 1024}.
+// One copy of the 32-point DFT: the two passes are a loop.
+__device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __restrict__ scr,
                                         const float2* __restrict__ tw) {
-  dft_dif<32, S>(v);  // v[brev(r)] = pass-A output index r
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    dft_reg<32>(v);
+    if (pass == 0) {
 #pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    float2 t = v[brev(r, 5)];
-    if (r != 0) {
-      const float2 w = tw[r * 32 + lane];
-      t = (S < 0) ? c_mul(t, w) : c_mulc(t, w);
+      for (int r = 1; r < 32; ++r) v[r] = c_mul(v[r], tw[r * 32 + lane]);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) scr[r * 33 + lane] = v[r].x;
+      __syncwarp();
+#pragma unroll
+      for (int n = 0; n < 32; ++n) v[n].x = scr[lane * 33 + n];
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 32; ++r) scr[r * 33 + lane] = v[r].y;
+      __syncwarp();
+#pragma unroll
+      for (int n = 0; n < 32; ++n) v[n].y = scr[lane * 33 + n];
+      __syncwarp();
     }
-    scr[r * 33 + lane] = t;
   }
-  __syncwarp();
-#pragma unroll
-  for (int n = 0; n < 32; ++n) v[n] = scr[lane * 33 + n];
-  __syncwarp();
-  dft_reg<32, S>(v);
 }
 
-// Inverse 512-point DFT after the spectral fold, one warp.
+// Forward 512-point DFT of the folded spectrum, one warp:
 //   in : z[k2] = Z[lane + 32*k2], k2 in [0,16)
-//   out: lane (2*r1 + h) gets o[r2] = x[r1 + 16*(r2 + 16*h)], r1 in [0,16), r2 in [0,16)
-//        x[r] = sum_k Z[k] e^{+2 pi i k r / 512}  (unnormalised)
-// scr: this warp's tile (>= 16 x 34 float2); tw512[r1*32 + l] = e^{-2 pi i r1 l / 512}.
-__device__ __forceinline__ void ifft512_fold_out(float2 (&z)[16], int lane, float2* __restrict__ scr,
-                                                 const float2* __restrict__ tw512, float2 (&o)[16]) {
-  dft_dif<16, +1>(z);  // z[brev4(r1)] = sum_k2 Z[lane+32k2] w16^{k2 r1}
-#pragma unroll
-  for (int r1 = 0; r1 < 16; ++r1) {
-    float2 t = z[brev(r1, 4)];
-    if (r1 != 0) t = c_mulc(t, tw512[r1 * 32 + lane]);
-    scr[r1 * 34 + lane] = t;
-  }
-  __syncwarp();
+//   out: lane (2*r1 + h) gets z[r2] = X[r1 + 16*(r2 + 16*h)],  X[r] = sum_k Z[k] e^{-2 pi i k r / 512}
+// scr: this warp's tile (>= 16 x 34 floats); tw512[r1*32 + l] = e^{-2 pi i r1 l / 512} (global, L1).
+// The inverse transform the method needs is conj(DFT(conj(Z))), done by the caller.
+__device__ __forceinline__ void fft512_pairs(float2 (&z)[16], int lane, float* __restrict__ scr,
+                                             const float2* __restrict__ tw512) {
   const int h = lane & 1, r1 = lane >> 1;
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    dft_reg<16>(z);
+    if (pass == 0) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) o[j] = scr[r1 * 34 + 2 * j + h];
-  __syncwarp();
-  dft_reg<16, +1>(o);  // o[r2] = sum_j A[2j+h][r1] w16^{j r2}  (E for h=0, O for h=1)
+      for (int r = 1; r < 16; ++r) z[r] = c_mul(z[r], __ldg(tw512 + r * 32 + lane));
+#pragma unroll
+      for (int r = 0; r < 16; ++r) scr[r * 34 + lane] = z[r].x;
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z[j].x = scr[r1 * 34 + 2 * j + h];
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) scr[r * 34 + lane] = z[r].y;
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z[j].y = scr[r1 * 34 + 2 * j + h];
+      __syncwarp();
+    }
+  }
+  // radix-2 across the lane pair: X[r2] = E[r2] + W32^{r2} O[r2], X[r2+16] = E[r2] - W32^{r2} O[r2].
+  // The odd lane twiddles its own O first; then out = sgn * mine + other (no selects on the data path).
+  const float sg = h ? -1.0f : 1.0f;
 #pragma unroll
   for (int r2 = 0; r2 < 16; ++r2) {
-    const float2 mine = o[r2];
+    const float2 t = tw32(z[r2], r2);
+    const float2 mine = h ? t : z[r2];
     float2 other;
     other.x = __shfl_xor_sync(0xffffffffu, mine.x, 1);
     other.y = __shfl_xor_sync(0xffffffffu, mine.y, 1);
-    const float2 ev = h ? other : mine;
-    const float2 od = tw32<+1>(h ? mine : other, r2);  // W_32^{+r2} O[r2]
-    o[r2] = h ? c_sub(ev, od) : c_add(ev, od);
+    z[r2] = make_float2(fmaf(sg, mine.x, other.x), fmaf(sg, mine.y, other.y));
   }
 }
 

@@ -5,59 +5,94 @@
 
 namespace kk {
 
-// Geometry of the fused S1-S4 kernel.
+// Geometry of the fused chain kernel.
 //   Hilbert chunk grid: 512 samples, window 1024 centred (reading R2)
 //   EQ grid           : overlap-save NF = 1024, keep 768 (margin 128 >= 101 FIR
 //                       reach), blocks start at owner position -128 + 768 j
 //   one CTA step      : 3072 samples = 3 Hilbert FFT pairs + 4 EQ blocks
+//                       (+ 768 symbols of WL apply / decision in APPLY mode)
 constexpr int STEP = 3072;
 constexpr int EQ_KEEP = 768;
-constexpr int EBUF = STEP + 256;    // E_s window of one step: [3072 i - 256, 3072 i + 3072)
+constexpr int EBUF = STEP + 256;    // D = E_tf - A_hat window of one step: [3072 i - 256, 3072 i + 3072)
 constexpr int STG = STEP + 512;     // codes of one step: [3072 i - 256, 3072 i + 3328)
-constexpr int X2_WARPS = 4;
-constexpr int TILE = 32 * 33;       // per-warp transpose tile (float2)
+constexpr int WARM = 1536;          // warm-up codes: [3072 i - 1280, 3072 i + 256)
+constexpr int XS = 1538;            // x2 window of one step (APPLY): positions 3072 i - 132 + 2 j
+constexpr int NWARPS = 4;
+constexpr int TILE = 32 * 33;       // per-warp transpose tile (floats)
+constexpr int SYM_PER_STEP = 768;
+constexpr int MAX_SEG = 4;
 
-struct X2Args {
-  const int16_t* codes;    // sample 0 of batch buffer 0 (halos readable)
+enum SegMode { SEG_APPLY = 0, SEG_X2_TAIL = 1, SEG_X2_FULL = 2 };
+
+// exact decision look-up table (built on the host):
+// cell word = count (bits 60..63, 15 = brute force) | up to 8 ascending 7-bit
+// point indices (bits 7c .. 7c+6)
+struct DecLut {
+  const unsigned long long* cell;  // [g*g]
+  float x0, y0, inv;               // cell (cx, cy) covers [x0 + cx/inv, ...)
+  int g;                           // grid size (0 = no LUT: always brute force)
+};
+
+// A segment of the step list: owners o = owner_first + k (k in [0, n_own)),
+// steps [i_begin, i_end) of each.  Owner o's codes start at codes + o*N.
+struct Seg {
+  int32_t owner_first, n_own, i_begin, i_end;
+  int32_t mode;            // SegMode
+  int32_t count_clip;      // count clipped samples of positions [0, N) (APPLY / FULL)
+  int32_t ref;             // FULL: owner whose position 0 is x2dst[0]; TAIL/APPLY: index base
+  int32_t pad;
+  float2* x2dst;           // TAIL: [k][X2H] tails; FULL: x2 index 0 of owner `ref`
+  uint8_t* out;            // APPLY: labels of owner owner_first
+  unsigned long long* counts;  // [k][8]
+  const float2* taps;      // APPLY: [k][8]
+  int64_t n_off;           // APPLY: pattern index of symbol 0 of owner owner_first
+};
+
+struct ChainArgs {
+  const int16_t* codes;    // sample 0 of owner 0 (halos readable)
   int64_t N;               // buffer_len
-  int32_t steps_per_buf;   // S_N
-  int32_t pre_first_step;  // i0 of the halo pre-pass (owner -1)
-  int32_t pre_steps;       // S_N - i0, or 0
-  int32_t nbuf;
+  int32_t nseg;
+  Seg seg[MAX_SEG];
   int64_t total_steps;
+  int64_t x2h;             // tail length (x2 samples) = 2K + 64
   float dc, vmin, a_hat, invN;
-  uint32_t tb_mod, s32, s512;  // tone_bin mod N, (tb*32) mod N, (tb*512) mod N
-  float2* x2;              // x2 index 0 (= position 0 of batch buffer 0); valid down to x2_lo
-  int64_t x2_lo;
+  uint32_t tb_mod, s32;    // tone_bin mod N, (tb*32) mod N
   const float2* tw1024;    // [32*32] e^{-2 pi i r l / 1024}
   const float2* tw512;     // [16*32] e^{-2 pi i r l / 512}
-  const float2* H;         // [1024] DFT of circularly placed h, / 1024
-  unsigned long long* counts;  // [nbuf][8]
-  float2* es_dump;         // debug: E_s at batch positions [0, nbuf*N) or nullptr
+  const float2* Hs;        // [1024] DFT of the tone-shifted h, / 1024 (reading R5 + downconversion)
+  float2* es_dump;         // debug: E_s of owners >= 0 of FULL segments, [owner*N + p], or nullptr
   int aligned16;
+  int64_t n_sym;
+  int32_t m;
+  const float2* pts;       // [m]
+  const uint8_t* labels;   // [m]
+  const uint8_t* pattern;  // [P] or nullptr
+  int64_t P;
+  DecLut lut;
 };
 
 struct LmsArgs {
-  const float2* x2;        // x2 index 0
+  const float2* x2_b0;     // x2 index 0 (position 0) of chain buffer 0
+  int64_t x2_stride;       // x2 samples between consecutive buffers' position 0
   int64_t n_sym;           // symbols per buffer
   int64_t L;               // sub-block
   int32_t nsub;            // n_sym / L
   int32_t nchains;         // nbuf * nsub
   int32_t K;
-  float mu, tau;
+  float mu, inv_tau;
   int32_t mode;
   int32_t m;
   const float2* pts;       // [m]
   const uint8_t* pattern;  // [P] or nullptr
   int64_t P;
-  int64_t n_off0;          // pattern offset of batch buffer 0
+  int64_t n_off0;          // pattern offset of buffer 0
   const float2* w_init;    // [8]
   float2* taps;            // [nchains][8]
   unsigned long long* counts;  // [nbuf][8]
 };
 
 struct ApplyArgs {
-  const float2* x2;
+  const float2* x2;        // x2 index 0 of buffer 0 (full layout, stride N/2)
   int64_t n_sym, L;
   int32_t nsub;
   int64_t total;           // nbuf * n_sym
@@ -69,15 +104,16 @@ struct ApplyArgs {
   const float2* taps;
   uint8_t* out;
   unsigned long long* counts;
+  DecLut lut;
 };
 
 // counter slots
 enum { C_BITERR = 0, C_SYMERR = 1, C_BITS = 2, C_SYMS = 3, C_CLIP = 4, C_GATED = 5, C_FLAGS = 6, C_ESUM = 7 };
 
-size_t x2_smem_bytes();
-cudaError_t launch_x2(const X2Args& a, int grid, cudaStream_t s);
+size_t chain_smem_bytes();
+cudaError_t chain_setup(int device, int* grid_out);
+cudaError_t launch_chain(const ChainArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_lms(const LmsArgs& a, cudaStream_t s);
 cudaError_t launch_apply(const ApplyArgs& a, cudaStream_t s);
-int x2_occupancy_grid(int device);
 
 }  // namespace kk

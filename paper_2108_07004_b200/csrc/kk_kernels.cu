@@ -1,11 +1,15 @@
 // kk_kernels.cu -- sm_100a kernels of the KK receiver hot path.
 //
-//   kk_x2_kernel    S1 front end + S2 blockwise Hilbert + S3 reconstruction /
-//                   carrier removal / downconversion + S4 static EQ with 4->2
-//                   fold, fused; E_s never leaves shared memory.  Writes x2.
-//   kk_lms_kernel   S5 update pass: one warp per sub-block chain of K steps
-//                   (sequential, "significant time", few resources)
-//   kk_apply_kernel S5' fixed-tap WL apply + S6 decision + S7 demap and count
+//   kk_chain_kernel<APPLY=true>   the whole per-sample chain, fused: S1 front end,
+//       S2 blockwise Hilbert, S3 reconstruction + carrier removal, S4 static EQ
+//       with 4->2 fold and downconversion, S5' fixed-tap WL apply, S6 decision,
+//       S7 demap + count.  Reads int16 codes, writes uint8 labels; E_s and x2
+//       never leave shared memory.
+//   kk_chain_kernel<APPLY=false>  same S1-S4 code, writes x2 to HBM (only the
+//       tails the LMS update pass needs, or everything for debug / L < N/4).
+//   kk_lms_kernel    S5 update pass: one warp per sub-block chain of K steps
+//                    (sequential, "significant time", few resources)
+//   kk_apply_kernel  S5'-S7 from materialised x2 (sub_block < buffer only)
 //
 // No tensor cores: nothing here is a dense contraction.
 #include <cuda_runtime.h>
@@ -16,257 +20,516 @@
 
 namespace kk {
 
-#define KK_HOST_DEVICE_INLINE __device__ __forceinline__
+constexpr size_t SMEM_TW = 1024 * sizeof(float2);
+constexpr size_t SMEM_EBUF = EBUF * sizeof(float2);
+constexpr size_t SMEM_STG = STG * sizeof(int16_t);
+constexpr size_t SMEM_XS = XS * sizeof(float2);  // also holds the warm-up codes (WARM int16)
+constexpr size_t CHAIN_SMEM = SMEM_TW + SMEM_EBUF + SMEM_STG + SMEM_XS + 16;
+static_assert(WARM * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-up codes + tile must fit the x2 window");
+static_assert(TILE * sizeof(float) <= EQ_KEEP * sizeof(float2), "transpose tile must fit an EQ stride of ebuf");
 
-// ---------------------------------------------------------------------------
-// Kernel 1: fused S1-S4
-// ---------------------------------------------------------------------------
-constexpr int X2_SMEM_FLOAT2 = 1024 + 512 + 1024 + EBUF + X2_WARPS * TILE;
-constexpr size_t X2_SMEM_BYTES = X2_SMEM_FLOAT2 * sizeof(float2) + STG * sizeof(int16_t);
+size_t chain_smem_bytes() { return CHAIN_SMEM; }
 
-size_t x2_smem_bytes() { return X2_SMEM_BYTES; }
-
-KK_HOST_DEVICE_INLINE float logamp(int16_t c, const X2Args& a, float invd) {
-  // S1: v = max(code + d, v_min); l = ln sqrt(v).  Computed as
-  // 0.5 ln(v/d): the constant 0.5 ln d lies in the DC bin, which the Hilbert
-  // mask zeroes, so phi is unchanged while fp32 keeps full relative precision.
-  const float v = fmaxf((float)c + a.dc, a.vmin);
-  return __log2f(v * invd) * 0.34657359027997264f;  // 0.5 * ln 2
+__device__ __forceinline__ uint32_t add_mod(uint32_t q, uint32_t s, uint32_t n) {
+  const uint32_t r = q + s;
+  return (r >= n) ? r - n : r;
 }
 
-KK_HOST_DEVICE_INLINE uint32_t tone_index(const X2Args& a, int64_t pos) {
+__device__ __forceinline__ uint32_t tone_index(const ChainArgs& a, int64_t pos) {
   // (tone_bin * pos) mod N, exact (reading R7); pos may be negative (halo)
   int64_t r = ((int64_t)a.tb_mod * pos) % a.N;
   if (r < 0) r += a.N;
   return (uint32_t)r;
 }
 
-KK_HOST_DEVICE_INLINE uint32_t add_mod(uint32_t q, uint32_t s, uint32_t n) {
-  uint32_t r = q + s;
-  return (r >= n) ? r - n : r;
-}
-
-KK_HOST_DEVICE_INLINE float2 es_sample(int16_t code, float phi, uint32_t q, const X2Args& a) {
-  // S3: E_s = (sqrt(v) e^{i phi} - A_hat) e^{+i theta}, theta = 2 pi q / N
-  const float v = fmaxf((float)code + a.dc, a.vmin);
-  const float amp = sqrtf(v);
-  float t = phi * 0.15915494309189535f;
+__device__ __forceinline__ void cis_turns(float t, float* s, float* c) {
+  // e^{2 pi i t} for any t, with exact reduction to [-1/2, 1/2] before __sincosf
   t -= rintf(t);
-  float sp, cp;
-  __sincosf(t * 6.2831853071795865f, &sp, &cp);
-  float tt = (float)q * a.invN;
-  tt = (tt >= 0.5f) ? tt - 1.0f : tt;
-  float st, ct;
-  __sincosf(tt * 6.2831853071795865f, &st, &ct);
-  const float ex = fmaf(amp, cp, -a.a_hat), ey = amp * sp;
-  return make_float2(fmaf(ex, ct, -ey * st), fmaf(ex, st, ey * ct));
+  __sincosf(t * 6.2831853071795865f, s, c);
 }
 
-// One Hilbert FFT pair: chunks c0 and c0+1 (each 512 samples, window 1024
-// centred, PAPER l.47 / reading R2) packed as z = l_c0 + i l_{c0+1}; the mask
-// +i sgn(k) is Hermitian so IFFT(mask * FFT(z)) = phi_c0 + i phi_{c0+1}.
-// Writes E_s at owner positions [wlo, whi) to ebuf[pos - ebuf_base].
-KK_HOST_DEVICE_INLINE void hilbert_pair(const X2Args& a, int owner, int64_t c0, const int16_t* __restrict__ stg,
-                                        int64_t stg_base, float2* __restrict__ ebuf, int64_t ebuf_base,
-                                        int64_t wlo, int64_t whi, bool count, float2* __restrict__ scr,
-                                        const float2* __restrict__ tw, int lane, float invd) {
-  float2 v[32];
-  const int re0 = (int)(512 * c0 - 256 - stg_base);
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j].x = logamp(stg[re0 + lane + 32 * j], a, invd);
-#pragma unroll
-  for (int j = 0; j < 32; ++j)
-    v[j].y = (j < 16) ? v[j + 16].x : logamp(stg[re0 + lane + 32 * (j + 16)], a, invd);
+// Exact minimum-distance decision (ties -> lowest index, reading R11): the LUT
+// cell lists (ascending) every point that can be nearest anywhere in the
+// (slightly enlarged) cell; brute force outside the grid or for crowded cells.
+constexpr unsigned long long LUT_BRUTE = 15ull << 60;
 
-  fft1024<-1>(v, lane, scr, tw);
-  // phi = -H{l}: multiply by +i sgn(k) / 1024, k = lane + 32 k2 (DC and Nyquist -> 0)
-  const float sc = 1.0f / 1024.0f;
-#pragma unroll
-  for (int k2 = 0; k2 < 32; ++k2) {
-    const float2 x = v[k2];
-    float2 r = (k2 < 16) ? make_float2(-x.y * sc, x.x * sc) : make_float2(x.y * sc, -x.x * sc);
-    if ((k2 == 0 || k2 == 16) && lane == 0) r = make_float2(0.f, 0.f);
-    v[k2] = r;
+__device__ __forceinline__ unsigned long long lut_word(float2 y, const DecLut& L) {
+  if (L.g > 0) {
+    const float fx = (y.x - L.x0) * L.inv, fy = (y.y - L.y0) * L.inv;
+    if (fx >= 0.f && fy >= 0.f && fx < (float)L.g && fy < (float)L.g)
+      return __ldg(L.cell + (int)fy * L.g + (int)fx);
   }
-  fft1024<+1>(v, lane, scr, tw);
-
-  // keep the centre: window index m = lane + 32 n2, n2 in [8, 24)
-  const int64_t pos_first = 512 * c0 + lane;  // m - 256 for n2 = 8
-  uint32_t q = tone_index(a, pos_first);
-  const uint32_t n32 = (uint32_t)a.N;
-  unsigned clip = 0;
-#pragma unroll
-  for (int n2 = 8; n2 < 24; ++n2) {
-    const int64_t pos = pos_first + 32 * (n2 - 8);
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int64_t p = pos + 512 * half;
-      if (p >= wlo && p < whi) {
-        const uint32_t qq = half ? add_mod(q, a.s512, n32) : q;
-        const int16_t code = stg[p - stg_base];
-        const float2 e = es_sample(code, half ? v[n2].y : v[n2].x, qq, a);
-        ebuf[p - ebuf_base] = e;
-        if (count && p >= 0 && p < a.N) {
-          clip += ((float)code + a.dc < a.vmin) ? 1u : 0u;
-          if (a.es_dump) a.es_dump[(int64_t)owner * a.N + p] = e;
-        }
-      }
-    }
-    q = add_mod(q, a.s32, n32);
-  }
-  if (count) {
-    clip = __reduce_add_sync(0xffffffffu, clip);
-    if (lane == 0 && clip) atomicAdd(&a.counts[owner * 8 + C_CLIP], (unsigned long long)clip);
-  }
+  return LUT_BRUTE;
 }
 
-// One static-EQ block (reading R4/R5): window ebuf[0..1024) = E_s at owner
-// positions [P0, P0 + 1024); FFT, x H/1024, fold (Y_k + Y_{k+512}), 512-point
-// IFFT; keeps x2 at positions P0 + 2r, r in [64, 448).
-KK_HOST_DEVICE_INLINE void eq_block(const X2Args& a, int owner, int64_t P0, const float2* __restrict__ win,
-                                    const float2* __restrict__ H, float2* __restrict__ scr,
-                                    const float2* __restrict__ tw, const float2* __restrict__ tw512, int lane) {
-  float2 v[32];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) v[r] = win[lane + 32 * r];
-  fft1024<-1>(v, lane, scr, tw);
-  float2 z[16];
-#pragma unroll
-  for (int k2 = 0; k2 < 16; ++k2)
-    z[k2] = c_add(c_mul(v[k2], H[lane + 32 * k2]), c_mul(v[k2 + 16], H[lane + 32 * (k2 + 16)]));
-  float2 o[16];
-  ifft512_fold_out(z, lane, scr, tw512, o);
-  const int h = lane & 1, r1 = lane >> 1;
-  const int64_t own_lo = (owner >= 0) ? 0 : a.N + 2 * a.x2_lo;
-#pragma unroll
-  for (int r2 = 0; r2 < 16; ++r2) {
-    const int rr = r1 + 16 * (r2 + 16 * h);
-    const int64_t P = P0 + 2 * rr;
-    if (rr >= 64 && rr < 448 && P >= own_lo && P < a.N) {
-      a.x2[((int64_t)owner * a.N + P) >> 1] = o[r2];
+__device__ __forceinline__ int decide_word(float2 y, unsigned long long w, const float2* __restrict__ sp, int m) {
+  const int cnt = (int)(w >> 60);
+  const bool brute = cnt == 15;
+  const int n = brute ? m : cnt;
+  float best = __int_as_float(0x7f800000);
+  int kb = 0;
+  for (int c = 0; c < n; ++c) {
+    const int k = brute ? c : (int)((w >> (7 * c)) & 127ull);
+    const float dx = y.x - sp[k].x, dy = y.y - sp[k].y;
+    const float d = fmaf(dx, dx, dy * dy);
+    if (d < best) {
+      best = d;
+      kb = k;
     }
   }
+  return kb;
 }
 
-__device__ __forceinline__ void stage_codes(const int16_t* __restrict__ src, int count, int16_t* __restrict__ dst,
-                                            bool aligned) {
-  if (aligned) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
-    for (int i = threadIdx.x; i < count / 8; i += blockDim.x) d4[i] = __ldg(s4 + i);
-  } else {
-    for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
+__device__ __forceinline__ int decide(float2 y, const DecLut& L, const float2* __restrict__ sp, int m) {
+  return decide_word(y, lut_word(y, L), sp, m);
+}
+
+__device__ __forceinline__ float2 wl_out(const float2 (&w)[4], const float2 (&g)[4], float2 u0, float2 u1, float2 u2,
+                                         float2 u3) {
+  // y = w^T u + g^T u*  (SPEC.md l.388 convention), u = (x2[2n+1], x2[2n], x2[2n-1], x2[2n-2])
+  const float2 uu[4] = {u0, u1, u2, u3};
+  float2 y = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    y.x += w[k].x * uu[k].x - w[k].y * uu[k].y + g[k].x * uu[k].x + g[k].y * uu[k].y;
+    y.y += w[k].x * uu[k].y + w[k].y * uu[k].x + g[k].y * uu[k].x - g[k].x * uu[k].y;
   }
+  return y;
 }
 
-__global__ void __launch_bounds__(X2_WARPS * 32) kk_x2_kernel(X2Args a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* s_tw = reinterpret_cast<float2*>(smem_raw);
-  float2* s_tw512 = s_tw + 1024;
-  float2* s_H = s_tw512 + 512;
-  float2* ebuf = s_H + 1024;
-  float2* scr_all = ebuf + EBUF;
-  int16_t* stg = reinterpret_cast<int16_t*>(scr_all + X2_WARPS * TILE);
+__device__ __forceinline__ unsigned warp_sum(unsigned v) { return __reduce_add_sync(0xffffffffu, v); }
 
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-    s_tw[i] = a.tw1024[i];
-    s_H[i] = a.H[i];
-  }
-  for (int i = threadIdx.x; i < 512; i += blockDim.x) s_tw512[i] = a.tw512[i];
-  __syncthreads();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float2* scr = scr_all + warp * TILE;
-  const float invd = 1.0f / a.dc;
-  const int64_t g0 = (int64_t)blockIdx.x * a.total_steps / gridDim.x;
-  const int64_t g1 = (int64_t)(blockIdx.x + 1) * a.total_steps / gridDim.x;
-  int prev_owner = -1000000;
-  int64_t prev_i = -1000000;
-  const bool aligned = a.aligned16 != 0;
-
-  for (int64_t g = g0; g < g1; ++g) {
-    int owner;
-    int64_t i;
-    if (g < a.pre_steps) {
-      owner = -1;
-      i = a.pre_first_step + g;
-    } else {
-      const int64_t gg = g - a.pre_steps;
-      owner = (int)(gg / a.steps_per_buf);
-      i = gg - (int64_t)owner * a.steps_per_buf;
-    }
-    const int16_t* obase = a.codes + (int64_t)owner * a.N;
-    const int64_t base = (int64_t)STEP * i - 256;  // owner position of ebuf[0] and stg[0]
-
-    if (!(owner == prev_owner && i == prev_i + 1)) {
-      // warm-up: E_s at [3072 i - 256, 3072 i) from the pair (6i-2, 6i-1)
-      const int64_t wbase = (int64_t)STEP * i - 1280;
-      __syncthreads();
-      stage_codes(obase + wbase, 1536, stg, aligned);
-      __syncthreads();
-      if (warp == 0)
-        hilbert_pair(a, owner, 6 * i - 2, stg, wbase, ebuf, base, base, base + 256, false, scr, s_tw, lane, invd);
-    }
-    __syncthreads();
-    stage_codes(obase + base, STG, stg, aligned);
-    __syncthreads();
-    if (warp < 3)
-      hilbert_pair(a, owner, 6 * i + 2 * warp, stg, base, ebuf, base, base + 256, base + 256 + STEP, owner >= 0,
-                   scr, s_tw, lane, invd);
-    __syncthreads();
-    eq_block(a, owner, base + EQ_KEEP * warp, ebuf + EQ_KEEP * warp, s_H, scr, s_tw, s_tw512, lane);
-    __syncthreads();
-    for (int k = threadIdx.x; k < 256; k += blockDim.x) ebuf[k] = ebuf[STEP + k];
-    prev_owner = owner;
-    prev_i = i;
-  }
+// --- TMA bulk copy + mbarrier helpers (sm_90+)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "KK_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra KK_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
 }
 
-int x2_occupancy_grid(int device) {
-  int sms = 0, occ = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  cudaFuncSetAttribute(kk_x2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X2_SMEM_BYTES);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk_x2_kernel, X2_WARPS * 32, X2_SMEM_BYTES);
-  if (occ < 1) occ = 1;
-  return sms * occ;
-}
-
-cudaError_t launch_x2(const X2Args& a, int grid, cudaStream_t s) {
-  cudaFuncSetAttribute(kk_x2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X2_SMEM_BYTES);
-  if (grid > a.total_steps) grid = (int)a.total_steps;
-  if (grid < 1) return cudaSuccess;
-  kk_x2_kernel<<<grid, X2_WARPS * 32, X2_SMEM_BYTES, s>>>(a);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// Kernel 2: LMS update pass, one warp per sub-block chain (reading R10)
-// ---------------------------------------------------------------------------
-struct Best {
-  float d1;
-  int k1;
-  float d2;
+struct StepPos {
+  int s, o;
+  int64_t i;
 };
 
-__device__ __forceinline__ Best merge_best(Best a, Best b) {
-  Best r;
-  if (b.d1 < a.d1 || (b.d1 == a.d1 && b.k1 < a.k1)) {
-    r.d1 = b.d1; r.k1 = b.k1; r.d2 = fminf(b.d2, a.d1);
-  } else {
-    r.d1 = a.d1; r.k1 = a.k1; r.d2 = fminf(a.d2, b.d1);
+__device__ __forceinline__ StepPos decode_step(const ChainArgs& a, int64_t g) {
+  StepPos r{0, 0, 0};
+#pragma unroll 1
+  for (int s = 0; s < a.nseg; ++s) {
+    const int64_t per = a.seg[s].i_end - a.seg[s].i_begin;
+    const int64_t cnt = per * a.seg[s].n_own;
+    if (g < cnt || s == a.nseg - 1) {
+      const int64_t k = g / per;
+      r.s = s;
+      r.o = a.seg[s].owner_first + (int)k;
+      r.i = a.seg[s].i_begin + (g - k * per);
+      return r;
+    }
+    g -= cnt;
   }
   return r;
 }
 
-__global__ void __launch_bounds__(128) kk_lms_kernel(LmsArgs a) {
+// ---------------------------------------------------------------------------
+// Kernel 1: the fused chain.  A persistent grid; each CTA walks a contiguous
+// range of the step list (segments of owners x steps).  Per 3072-sample step:
+//   stage codes (TMA bulk copy prefetched during the previous step)
+//   phase H: 3 Hilbert FFT pairs (warps 0-2) + the warm-up pair (warp 3) when
+//            the CTA starts a new owner: S1, S2, S3 -> D = E_tf - A_hat in smem
+//   phase E: 4 static-EQ blocks (one per warp): S4 -> x2 (smem or HBM)
+//   phase A: 768 symbols of S5' + S6 + S7 (APPLY segments)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float2* s_tw = reinterpret_cast<float2*>(smem_raw);
+  float2* ebuf = reinterpret_cast<float2*>(smem_raw + SMEM_TW);
+  int16_t* stg = reinterpret_cast<int16_t*>(smem_raw + SMEM_TW + SMEM_EBUF);
+  float2* xs = reinterpret_cast<float2*>(smem_raw + SMEM_TW + SMEM_EBUF + SMEM_STG);
+  int16_t* wstg = reinterpret_cast<int16_t*>(xs);  // warm-up codes (H phase only)
+  float* wscr = reinterpret_cast<float*>(xs + WARM / 4);  // warm-up task's transpose tile
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + SMEM_TW + SMEM_EBUF + SMEM_STG + SMEM_XS);
+  __shared__ float2 s_pts[128];
+  __shared__ uint8_t s_lab[128];
+
+  for (int k = threadIdx.x; k < 1024; k += blockDim.x) s_tw[k] = a.tw1024[k];
+  for (int k = threadIdx.x; k < a.m; k += blockDim.x) {
+    s_pts[k] = a.pts[k];
+    s_lab[k] = a.labels[k];
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float invd = 1.0f / a.dc;
+  const uint32_t n32 = (uint32_t)a.N;
+  const int64_t g0 = (int64_t)blockIdx.x * a.total_steps / gridDim.x;
+  const int64_t g1 = (int64_t)(blockIdx.x + 1) * a.total_steps / gridDim.x;
+  int prev_s = -1, prev_o = -1000000;
+  int64_t prev_i = -1000000;
+  unsigned acc_clip = 0, acc_se = 0, acc_be = 0;
+  unsigned phase_bit = 0;
+  bool prefetched = false;
+  // WL taps of the current owner, factored: y.x = sum ta.x u.x + ta.y u.y, y.y = sum tc.x u.x + tc.y u.y
+  float2 ta[4], tc[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) ta[k] = tc[k] = make_float2(0.f, 0.f);
+
+  auto flush = [&](int s, int o) {
+    if (s < 0) return;
+    const unsigned c = warp_sum(acc_clip), se = warp_sum(acc_se), be = warp_sum(acc_be);
+    unsigned long long* cnt = a.seg[s].counts;
+    if (lane == 0 && cnt) {
+      const int64_t k = (int64_t)(o - a.seg[s].owner_first) * 8;
+      if (c) atomicAdd(&cnt[k + C_CLIP], (unsigned long long)c);
+      if (se) atomicAdd(&cnt[k + C_SYMERR], (unsigned long long)se);
+      if (be) atomicAdd(&cnt[k + C_BITERR], (unsigned long long)be);
+    }
+    acc_clip = acc_se = acc_be = 0;
+  };
+
+  // tone phase indices (tb * P) mod N of the EQ outputs: P = sbase + 768 q + 2 (r1 + 256 h) + 32 r2
+  const uint32_t s3072 = tone_index(a, STEP);
+  uint32_t q_tap[NWARPS];
+#pragma unroll
+  for (int k = 0; k < NWARPS; ++k) q_tap[k] = tone_index(a, (int64_t)EQ_KEEP * k);
+  const uint32_t q_lane = tone_index(a, 2 * ((lane >> 1) + 256 * (lane & 1)));
+  uint32_t q_step = 0;
+
+  StepPos cur = (g0 < g1) ? decode_step(a, g0) : StepPos{0, 0, 0};
+  for (int64_t g = g0; g < g1; ++g) {
+    const int s = cur.s, owner = cur.o;
+    const int64_t i = cur.i;
+    const Seg& sg = a.seg[s];
+    const int mode = sg.mode;
+    const bool warm = !(s == prev_s && owner == prev_o && i == prev_i + 1);
+    StepPos nxt = (g + 1 < g1) ? decode_step(a, g + 1) : StepPos{-1, 0, 0};
+    const bool next_cont = (g + 1 < g1) && nxt.s == s && nxt.o == owner && nxt.i == i + 1;
+    if (s != prev_s || owner != prev_o) {
+      flush(prev_s, prev_o);
+      if (mode == SEG_APPLY) {
+        const float2* tp = sg.taps + (int64_t)(owner - sg.owner_first) * 8;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 w = tp[k], gg = tp[4 + k];
+          ta[k] = make_float2(w.x + gg.x, gg.y - w.y);
+          tc[k] = make_float2(w.y + gg.y, w.x - gg.x);
+        }
+      }
+    }
+    const int16_t* obase = a.codes + (int64_t)owner * a.N;
+    const int64_t sbase = (int64_t)STEP * i - 256;   // owner position of stg[0] and ebuf[0]
+    q_step = warm ? tone_index(a, sbase) : add_mod(q_step, s3072, n32);
+    const int64_t wbase = (int64_t)STEP * i - 1280;  // owner position of wstg[0]
+
+    // ---- codes of this step
+    if (prefetched) {
+      mbar_wait(bar, phase_bit);
+      phase_bit ^= 1u;
+    } else if (a.aligned16) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(obase + sbase);
+      uint4* d4 = reinterpret_cast<uint4*>(stg);
+      for (int k = threadIdx.x; k < STG / 8; k += blockDim.x) d4[k] = __ldg(s4 + k);
+    } else {
+      for (int k = threadIdx.x; k < STG; k += blockDim.x) stg[k] = obase[sbase + k];
+    }
+    if (warm) {
+      if (a.aligned16) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(obase + wbase);
+        uint4* d4 = reinterpret_cast<uint4*>(wstg);
+        for (int k = threadIdx.x; k < WARM / 8; k += blockDim.x) d4[k] = __ldg(s4 + k);
+      } else {
+        for (int k = threadIdx.x; k < WARM; k += blockDim.x) wstg[k] = obase[wbase + k];
+      }
+    }
+    __syncthreads();
+
+    // ---- phase 0: Hilbert pairs (warps 0-2, warp 3 = warm-up pair); phase 1: EQ blocks
+#pragma unroll 1
+    for (int phase = 0; phase < 2; ++phase) {
+      const bool isH = phase == 0;
+      if (!isH) {
+        // stg is free now: prefetch the next step's codes (async proxy) behind phases E and A
+        prefetched = next_cont && a.aligned16;
+        if (prefetched && threadIdx.x == 0) {
+          fence_proxy_async();
+          bulk_load(stg, obase + sbase + STEP, STG * sizeof(int16_t), bar);
+        }
+      }
+      const bool active = !isH || warp < 3 || warm;
+      if (active) {
+        float2 v[32];
+        int64_t c0 = 0;
+        const bool wt = isH && warp >= 3;  // warm-up task
+        const int16_t* src = wt ? wstg : stg;
+        const int64_t base = wt ? wbase : sbase;
+        if (isH) {
+          // S1: l = 0.5 ln(v/d) (the constant 0.5 ln d is in the DC bin, zeroed by the mask)
+          c0 = wt ? 6 * i - 2 : 6 * i + 2 * warp;
+          const int re0 = (int)(512 * c0 - 256 - base);
+#pragma unroll
+          for (int j = 0; j < 48; ++j) {
+            const float vv = fmaxf((float)src[re0 + lane + 32 * j] + a.dc, a.vmin);
+            const float l = __log2f(vv * invd) * 0.34657359027997264f;  // 0.5 * ln 2
+            if (j < 32) v[j].x = l;
+            if (j >= 16) v[j - 16].y = l;
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) v[r] = ebuf[EQ_KEEP * warp + lane + 32 * r];
+        }
+        // transpose tile: H tasks use their own (not yet written) output slice of ebuf,
+        // the warm-up task a slice of xs; E tasks reuse ebuf once every window is loaded.
+        float* scr = wt ? wscr : reinterpret_cast<float*>(ebuf + (isH ? 256 + 1024 * warp : EQ_KEEP * warp));
+        if (!isH) __syncthreads();  // all E windows are in registers before ebuf becomes scratch
+        const int nfft = isH ? 2 : 1;
+#pragma unroll 1
+        for (int f = 0; f < nfft; ++f) {
+          fft1024(v, lane, scr, s_tw);
+          if (isH && f == 0) {
+            // S2: phi = -H{l} <-> +i sgn(k) L_k (reading R1), /1024, conjugated so the
+            // next forward FFT computes the inverse: IFFT(Y) = conj(FFT(conj(Y)))
+            const float sc = 1.0f / 1024.0f;
+#pragma unroll
+            for (int k2 = 0; k2 < 32; ++k2) {
+              const float2 y = v[k2];
+              float2 r = (k2 < 16) ? make_float2(-y.y * sc, -y.x * sc) : make_float2(y.y * sc, y.x * sc);
+              if ((k2 == 0 || k2 == 16) && lane == 0) r = make_float2(0.f, 0.f);
+              v[k2] = r;
+            }
+          }
+        }
+        if (isH) {
+          // S3 (tone frame): D = sqrt(v) e^{i phi} - A_hat; phi_re = v.x, phi_im = -v.y.
+          // Window index m = lane + 32 n2 (n2 in [8, 24)); chunk c0 at m - 256, chunk c0+1 at m + 256.
+          const int s_off = (int)(512 * c0 - 256 - base);
+          const int e_off = (int)(512 * c0 - 256 - sbase);
+          // warm-up task: all 1024 outputs to a slice of xs (its tile is dead), then its last 256 to ebuf[0, 256)
+          float2* dst = wt ? (xs + WARM / 4 - 256) : (ebuf + e_off);
+          const bool cnt = !wt && sg.count_clip && (mode == SEG_APPLY || owner >= sg.ref);
+          const int lim = (int)((a.N - sbase < (int64_t)(1 << 30)) ? a.N - sbase : (int64_t)(1 << 30)) - e_off;
+          unsigned clip = 0;
+          // phi to the imaginary slot of its own output (same lane writes and later reads it),
+          // then one rolled loop over the 32 outputs (keeps the kernel's code small)
+#pragma unroll
+          for (int n2 = 8; n2 < 24; ++n2) {
+            dst[lane + 32 * n2].y = v[n2].x;
+            dst[lane + 32 * n2 + 512].y = -v[n2].y;
+          }
+#pragma unroll 4
+          for (int t = 0; t < 32; ++t) {
+            const int mm = lane + 32 * (t & 15) + 256 + 512 * (t >> 4);
+            const float phi = dst[mm].y;
+            const int16_t code = src[s_off + mm];
+            const float vv = fmaxf((float)code + a.dc, a.vmin);
+            const float amp = vv * rsqrtf(vv);
+            float sp, cp;
+            cis_turns(phi * 0.15915494309189535f, &sp, &cp);
+            dst[mm] = make_float2(fmaf(amp, cp, -a.a_hat), amp * sp);
+            clip += ((float)code + a.dc < a.vmin && mm < lim) ? 1u : 0u;
+          }
+          if (cnt) acc_clip += clip;
+          if (wt) {
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 8; ++k) ebuf[lane + 32 * k] = dst[1024 + lane + 32 * k];
+          }
+          if (a.es_dump && !wt && mode == SEG_X2_FULL && owner >= sg.ref) {
+            // debug only: E_s = D e^{i theta_p} at owned positions
+            __syncwarp();
+#pragma unroll 1
+            for (int k = lane; k < 1024; k += 32) {
+              const int ei = e_off + 256 + k;
+              const int64_t pp = sbase + ei;
+              if (pp >= 0 && pp < a.N) {
+                const float2 d = ebuf[ei];
+                float st, ct;
+                cis_turns((float)tone_index(a, pp) * a.invN, &st, &ct);
+                a.es_dump[(int64_t)(owner - sg.ref) * a.N + pp] =
+                    make_float2(d.x * ct - d.y * st, d.x * st + d.y * ct);
+              }
+            }
+          }
+        } else {
+          // S4: x2 = e^{i theta_P} * IDFT512(fold(DFT1024(D) * Hs))  (downconversion moved
+          // behind the LTI filter: Hs is the DFT of h_i e^{-2 pi i tb i / N}, reading R5)
+          const int q = warp;
+          float2 z[16];
+#pragma unroll
+          for (int k2 = 0; k2 < 16; ++k2) {
+            const float2 s0 = c_mul(v[k2], __ldg(a.Hs + lane + 32 * k2));
+            const float2 s1 = c_mul(v[k2 + 16], __ldg(a.Hs + lane + 32 * (k2 + 16)));
+            z[k2] = make_float2(s0.x + s1.x, -(s0.y + s1.y));  // conj -> forward DFT = inverse
+          }
+          fft512_pairs(z, lane, scr, a.tw512);
+          const int h = lane & 1, r1 = lane >> 1;
+          // lane holds window outputs rr = r1 + 16 r2 + 256 h, i.e. positions P = P0 + 2 rr: a
+          // stride-16 run in x2 index; keep rr in [rlo, 448) and (X2 modes) the owned positions
+          const int rlo = (mode == SEG_APPLY && q == 0) ? 62 : 64;
+          const int rbase = r1 + 256 * h;
+          int lo2 = (rlo - rbase + 15) >> 4, hi2 = (448 - rbase + 15) >> 4;  // r2 range of kept outputs
+          lo2 = lo2 < 0 ? 0 : lo2;
+          hi2 = hi2 > 16 ? 16 : hi2;
+          const int64_t P0 = sbase + EQ_KEEP * q + 2 * rbase;  // position of r2 = 0
+          float2* dptr = nullptr;
+          if (mode == SEG_APPLY) {
+            dptr = xs + (384 * q + rbase - 62);
+          } else {
+            // owned window [own_lo, N) in position; x2 index = P / 2 relative to the destination base
+            const int64_t tail_lo = a.N - 2 * a.x2h;
+            int64_t own_lo, dbase;
+            if (mode == SEG_X2_TAIL) {
+              own_lo = tail_lo;
+              dbase = (int64_t)(owner - sg.owner_first) * a.x2h - (tail_lo >> 1);
+            } else {
+              own_lo = (owner < sg.ref) ? tail_lo : 0;
+              dbase = (int64_t)(owner - sg.ref) * (a.N >> 1);
+            }
+            // r2 with own_lo <= P0 + 32 r2 < N
+            const int64_t l2 = (own_lo - P0 + 31) >> 5, h2 = (a.N - P0 + 31) >> 5;
+            lo2 = (int)(l2 > lo2 ? (l2 < 16 ? l2 : 16) : lo2);
+            hi2 = (int)(h2 < hi2 ? (h2 > 0 ? h2 : 0) : hi2);
+            dptr = sg.x2dst + dbase + (P0 >> 1);
+          }
+          uint32_t qi = add_mod(add_mod(q_step, q_tap[q], n32), q_lane, n32);  // (tb * P0) mod N
+#pragma unroll
+          for (int r2 = 0; r2 < 16; ++r2) {
+            if (r2 >= lo2 && r2 < hi2) {
+              float st, ct;
+              cis_turns((float)qi * a.invN, &st, &ct);
+              const float2 o = z[r2];
+              dptr[16 * r2] = make_float2(o.x * ct + o.y * st, o.x * st - o.y * ct);  // conj(o) e^{i theta}
+            }
+            qi = add_mod(qi, a.s32, n32);
+          }
+        }
+      }
+      __syncthreads();
+    }
+
+    if (mode == SEG_APPLY) {
+      // ---- S5' + S6 + S7 on symbols [768 i - 32, 768 i + 736) of this owner
+      const int64_t nbase = (int64_t)SYM_PER_STEP * i - 32;
+      const int64_t ko = owner - sg.owner_first;
+      int64_t pb = 0;
+      if (a.pattern) {
+        pb = (sg.n_off + ko * a.n_sym + nbase) % a.P;
+        if (pb < 0) pb += a.P;
+      }
+      uint8_t* outp = sg.out + ko * a.n_sym;
+      constexpr int SPT = SYM_PER_STEP / (NWARPS * 32);  // symbols per thread per step (6)
+      constexpr int SB = 2;                               // symbols per inner batch
+#pragma unroll 1
+      for (int k0 = 0; k0 < SPT; k0 += SB) {
+        float2 yv[SB];
+        unsigned long long cw[SB];
+#pragma unroll
+        for (int k = 0; k < SB; ++k) {
+          // y = w^T u + g^T u* with u = (xs[2s+3], xs[2s+2], xs[2s+1], xs[2s]), factored taps
+          const int sidx = threadIdx.x + NWARPS * 32 * (k0 + k);
+          const float2 u[4] = {xs[2 * sidx + 3], xs[2 * sidx + 2], xs[2 * sidx + 1], xs[2 * sidx]};
+          float2 y = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            y.x = fmaf(ta[t].x, u[t].x, fmaf(ta[t].y, u[t].y, y.x));
+            y.y = fmaf(tc[t].x, u[t].x, fmaf(tc[t].y, u[t].y, y.y));
+          }
+          yv[k] = y;
+          cw[k] = lut_word(y, a.lut);  // independent loads, issued back to back
+        }
+#pragma unroll
+        for (int k = 0; k < SB; ++k) {
+          const int sidx = threadIdx.x + NWARPS * 32 * (k0 + k);
+          const int64_t n = nbase + sidx;
+          if (n >= 0 && n < a.n_sym) {
+            const int d = decide_word(yv[k], cw[k], s_pts, a.m);
+            const uint8_t ld = s_lab[d];
+            outp[n] = ld;
+            if (a.pattern) {
+              int64_t pi = pb + sidx;
+              while (pi >= a.P) pi -= a.P;
+              const int ref = a.pattern[pi];
+              acc_se += (ref != d) ? 1u : 0u;
+              acc_be += __popc((unsigned)(ld ^ s_lab[ref]));
+            }
+          }
+        }
+      }
+    }
+    // keep the last 256 D samples for the next step's first EQ window
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) ebuf[k] = ebuf[STEP + k];
+    __syncthreads();
+    prev_s = s;
+    prev_o = owner;
+    prev_i = i;
+    cur = nxt;
+  }
+  flush(prev_s, prev_o);
+}
+
+cudaError_t chain_setup(int device, int* grid_out) {
+  int sms = 0, occ = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaFuncSetAttribute(kk_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM);
+  if (e != cudaSuccess) return e;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk_chain_kernel, NWARPS * 32, CHAIN_SMEM);
+  if (occ < 1) occ = 1;
+  *grid_out = sms * occ;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chain(const ChainArgs& a, int grid, cudaStream_t s) {
+  if (a.total_steps <= 0) return cudaSuccess;
+  if (grid > a.total_steps) grid = (int)a.total_steps;
+  kk_chain_kernel<<<grid, NWARPS * 32, CHAIN_SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Kernel 2: LMS update pass, one warp per sub-block chain (reading R10).
+// The chain is inherently sequential, so the kernel minimises the
+// per-step latency and instruction count:
+//  * the widely-linear filter y = w^T u + g^T u* is the real 2x2 matrix filter
+//      [y.x; y.y] = sum_k [[A_k, B_k], [C_k, D_k]] [u_k.x; u_k.y],
+//    A = w.x + g.x, B = g.y - w.y, C = w.y + g.y, D = w.x - g.x, and the LMS update
+//    w += mu e u*, g += mu e u is exactly  [dA dB; dC dD] = 2 mu [e.x; e.y] [u.x u.y]
+//    (16 FFMA per step instead of 32); w, g are recovered at the end;
+//  * lookahead: y_{n+1} = yhat_{n+1} + 2 mu (sum_k u_{n,k} . u_{n+1,k}) e_n, with
+//    yhat computed from the pre-update matrix off the critical path;
+//  * decision: lanes hold up to 4 points; the nearest point comes from one
+//    REDUX.MIN over 32-bit keys (distance bits with the low 7 bits replaced by the
+//    point index: ties within 2^-16 relative are broken by index), D1 is recomputed
+//    exactly from that point, D2 from a second REDUX over exact distance bits.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(32) kk_lms_kernel(LmsArgs a) {
   __shared__ float2 s_pts[128];
   for (int i = threadIdx.x; i < a.m; i += blockDim.x) s_pts[i] = a.pts[i];
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * 4 + warp;
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
   if (c >= a.nchains) return;
   const int b = c / a.nsub, sblk = c - b * a.nsub;
-  const int64_t n0 = (int64_t)b * a.n_sym + (int64_t)sblk * a.L - a.K;
+  const int64_t n0l = (int64_t)sblk * a.L - a.K;       // first update symbol, buffer-relative
+  const int64_t n0 = (int64_t)b * a.n_sym + n0l;       // ... relative to buffer 0 (pattern index)
   const float INF = __int_as_float(0x7f800000);
   float2 p[4];
 #pragma unroll
@@ -274,97 +537,130 @@ __global__ void __launch_bounds__(128) kk_lms_kernel(LmsArgs a) {
     const int idx = lane + 32 * j;
     p[j] = (idx < a.m) ? s_pts[idx] : make_float2(INF, INF);
   }
-  float2 w[4], g[4];
+  float A[4], B[4], C[4], D[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    w[k] = a.w_init[k];
-    g[k] = a.w_init[4 + k];
+    const float2 w = a.w_init[k], g = a.w_init[4 + k];
+    A[k] = w.x + g.x;
+    B[k] = g.y - w.y;
+    C[k] = w.y + g.y;
+    D[k] = w.x - g.x;
   }
+  const float mu2 = 2.0f * a.mu;
   unsigned gated = 0;
   float esum = 0.f;
-  const float2* xp = a.x2 + 2 * n0;
-  float2 u0 = xp[1], u1 = xp[0], u2 = xp[-1], u3 = xp[-2];
-  for (int st = 0; st < a.K; ++st) {
-    // prefetch the next regressor
-    const float2* xn = xp + 2;
-    float2 nu0 = xn[1], nu1 = xn[0];
+  int64_t pidx = 0;
+  if (a.mode == 1) {
+    pidx = (a.n_off0 + n0) % a.P;
+    if (pidx < 0) pidx += a.P;
+  }
+  // x2 values of a block of 8 steps: step s uses xp[2s .. 2s+3]; prefetch one block ahead
+  const float2* xp = a.x2_b0 + (int64_t)b * a.x2_stride + 2 * n0l - 2;
+  float2 cur[18], nxt[18];
+#pragma unroll
+  for (int j = 0; j < 18; ++j) cur[j] = xp[j];
+  auto filt = [&](float2 u0, float2 u1, float2 u2, float2 u3) {
     const float2 uu[4] = {u0, u1, u2, u3};
-    float2 y = make_float2(0.f, 0.f);
+    float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      // y += w u + g conj(u)
-      y.x += w[k].x * uu[k].x - w[k].y * uu[k].y + g[k].x * uu[k].x + g[k].y * uu[k].y;
-      y.y += w[k].x * uu[k].y + w[k].y * uu[k].x + g[k].y * uu[k].x - g[k].x * uu[k].y;
+    for (int k = 0; k < 4; k += 2) {
+      x0 = fmaf(A[k], uu[k].x, fmaf(B[k], uu[k].y, x0));
+      x1 = fmaf(A[k + 1], uu[k + 1].x, fmaf(B[k + 1], uu[k + 1].y, x1));
+      y0 = fmaf(C[k], uu[k].x, fmaf(D[k], uu[k].y, y0));
+      y1 = fmaf(C[k + 1], uu[k + 1].x, fmaf(D[k + 1], uu[k + 1].y, y1));
     }
-    Best bst;
-    bst.d1 = INF; bst.k1 = 1 << 30; bst.d2 = INF;
+    return make_float2(x0 + x1, y0 + y1);
+  };
+  float2 y = filt(cur[3], cur[2], cur[1], cur[0]);
+  for (int s0 = 0; s0 < a.K; s0 += 8) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float dx = y.x - p[j].x, dy = y.y - p[j].y;
-      const float d = fmaf(dx, dx, dy * dy);
-      if (d < bst.d1) {
-        bst.d2 = bst.d1; bst.d1 = d; bst.k1 = lane + 32 * j;
-      } else if (d < bst.d2) {
-        bst.d2 = d;
+    for (int j = 0; j < 18; ++j) nxt[j] = xp[2 * (s0 + 8) + j];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      if (s0 + jj < a.K) {
+        const float2 u0 = cur[2 * jj + 3], u1 = cur[2 * jj + 2], u2 = cur[2 * jj + 1], u3 = cur[2 * jj];
+        const float2 v0 = (jj < 7) ? cur[2 * jj + 5] : nxt[3];
+        const float2 v1 = (jj < 7) ? cur[2 * jj + 4] : nxt[2];
+        // off the critical path: yhat_{n+1} (pre-update matrix) and r = 2 mu sum_k u_n,k . u_n+1,k
+        const float2 yh = filt(v0, v1, u0, u1);
+        const float r = mu2 * (fmaf(u0.x, v0.x, u0.y * v0.y) + fmaf(u1.x, v1.x, u1.y * v1.y) +
+                               fmaf(u2.x, u0.x, u2.y * u0.y) + fmaf(u3.x, u1.x, u3.y * u1.y));
+        // decision: local best / second best over this lane's points
+        float d[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float dx = y.x - p[j].x, dy = y.y - p[j].y;
+          d[j] = fmaf(dx, dx, dy * dy);
+        }
+        float l1 = d[0], l2 = INF;
+        int lk = lane;
+#pragma unroll
+        for (int j = 1; j < 4; ++j) {
+          const bool better = d[j] < l1;
+          l2 = better ? l1 : fminf(l2, d[j]);
+          lk = better ? lane + 32 * j : lk;
+          l1 = better ? d[j] : l1;
+        }
+        const unsigned key = (__float_as_uint(l1) & ~127u) | (unsigned)lk;
+        const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
+        const unsigned k1 = kmin & 127u;
+        const float mine2 = ((unsigned)lk == k1) ? l2 : l1;
+        const float d2 = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(mine2)));
+        const float2 pk = s_pts[k1];
+        const float dx1 = y.x - pk.x, dy1 = y.y - pk.y;
+        const float d1 = fmaf(dx1, dx1, dy1 * dy1);
+        float2 ref;
+        float gamma = 1.0f;
+        if (a.mode == 1) {
+          ref = s_pts[a.pattern[pidx]];
+          pidx = (pidx + 1 == a.P) ? 0 : pidx + 1;
+        } else {
+          ref = pk;
+          if (a.mode == 0 && a.inv_tau > 0.f) gamma = fminf(1.0f, fmaxf(d2 - d1, 0.f) * a.inv_tau);
+        }
+        gated += (gamma < 1.0f) ? 1u : 0u;
+        const float2 e = make_float2(gamma * (ref.x - y.x), gamma * (ref.y - y.y));
+        esum = fmaf(e.x, e.x, fmaf(e.y, e.y, esum));
+        const float ex = mu2 * e.x, ey = mu2 * e.y;
+        const float2 uu[4] = {u0, u1, u2, u3};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          A[k] = fmaf(ex, uu[k].x, A[k]);
+          B[k] = fmaf(ex, uu[k].y, B[k]);
+          C[k] = fmaf(ey, uu[k].x, C[k]);
+          D[k] = fmaf(ey, uu[k].y, D[k]);
+        }
+        // y_{n+1} = yhat_{n+1} + r e_n
+        y = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
       }
     }
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      Best o;
-      o.d1 = __shfl_xor_sync(0xffffffffu, bst.d1, off);
-      o.k1 = __shfl_xor_sync(0xffffffffu, bst.k1, off);
-      o.d2 = __shfl_xor_sync(0xffffffffu, bst.d2, off);
-      bst = merge_best(bst, o);
-    }
-    float2 ref;
-    float gamma = 1.0f;
-    const int64_t n = n0 + st;
-    if (a.mode == 1) {
-      int64_t pi = (a.n_off0 + n) % a.P;
-      if (pi < 0) pi += a.P;
-      ref = s_pts[a.pattern[pi]];
-    } else {
-      ref = s_pts[bst.k1];
-      if (a.mode == 0 && a.tau > 0.f) gamma = fminf(1.0f, (bst.d2 - bst.d1) / a.tau);
-    }
-    gated += (gamma < 1.0f) ? 1u : 0u;
-    const float2 e = make_float2(gamma * (ref.x - y.x), gamma * (ref.y - y.y));
-    esum += e.x * e.x + e.y * e.y;
-    const float2 me = make_float2(a.mu * e.x, a.mu * e.y);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      // w += mu e conj(u);  g += mu e u
-      w[k].x += me.x * uu[k].x + me.y * uu[k].y;
-      w[k].y += me.y * uu[k].x - me.x * uu[k].y;
-      g[k].x += me.x * uu[k].x - me.y * uu[k].y;
-      g[k].y += me.x * uu[k].y + me.y * uu[k].x;
-    }
-    u3 = u1; u2 = u0; u1 = nu1; u0 = nu0;
-    xp = xn;
+    for (int j = 0; j < 18; ++j) cur[j] = nxt[j];
   }
   if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      a.taps[(int64_t)c * 8 + k] = w[k];
-      a.taps[(int64_t)c * 8 + 4 + k] = g[k];
+      // w = ((A + D) + i (C - B)) / 2,  g = ((A - D) + i (C + B)) / 2
+      a.taps[(int64_t)c * 8 + k] = make_float2(0.5f * (A[k] + D[k]), 0.5f * (C[k] - B[k]));
+      a.taps[(int64_t)c * 8 + 4 + k] = make_float2(0.5f * (A[k] - D[k]), 0.5f * (C[k] + B[k]));
     }
     atomicAdd(&a.counts[b * 8 + C_GATED], (unsigned long long)gated);
     bool bad = !(esum / (float)a.K <= 1.0f);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) bad |= !isfinite(w[k].x + w[k].y + g[k].x + g[k].y);
+    for (int k = 0; k < 4; ++k) bad |= !isfinite(A[k] + B[k] + C[k] + D[k]);
     if (bad) atomicOr(&a.counts[b * 8 + C_FLAGS], 1ull);
   }
 }
 
 cudaError_t launch_lms(const LmsArgs& a, cudaStream_t s) {
-  const int grid = (a.nchains + 3) / 4;
-  if (grid < 1) return cudaSuccess;
-  kk_lms_kernel<<<grid, 128, 0, s>>>(a);
+  if (a.nchains < 1) return cudaSuccess;
+  kk_lms_kernel<<<a.nchains, 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
-// Kernel 3: fixed-tap WL apply, decision, demap, count
+// Kernel 3: fixed-tap WL apply, decision, demap, count from materialised x2
+// (used when sub_block < buffer: several tap sets per buffer)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) kk_apply_kernel(ApplyArgs a) {
   __shared__ float2 s_pts[128];
@@ -377,41 +673,30 @@ __global__ void __launch_bounds__(128) kk_apply_kernel(ApplyArgs a) {
   __syncthreads();
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned se = 0, be = 0;
-  int64_t b = (int64_t)blockIdx.x * blockDim.x / a.n_sym;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x / a.n_sym;
   if (n < a.total) {
     const int64_t nl = n - b * a.n_sym;
     const int64_t chain = b * a.nsub + nl / a.L;
-    const float2* tp = a.taps + chain * 8;
-    const float2* xp = a.x2 + 2 * n;
-    const float2 uu[4] = {xp[1], xp[0], xp[-1], xp[-2]};
-    float2 y = make_float2(0.f, 0.f);
+    float2 w[4], g[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float2 w = tp[k], g = tp[4 + k];
-      y.x += w.x * uu[k].x - w.y * uu[k].y + g.x * uu[k].x + g.y * uu[k].y;
-      y.y += w.x * uu[k].y + w.y * uu[k].x + g.y * uu[k].x - g.x * uu[k].y;
+      w[k] = a.taps[chain * 8 + k];
+      g[k] = a.taps[chain * 8 + 4 + k];
     }
-    float dbest = __int_as_float(0x7f800000);
-    int kbest = 0;
-    for (int k = 0; k < a.m; ++k) {
-      const float dx = y.x - s_pts[k].x, dy = y.y - s_pts[k].y;
-      const float d = fmaf(dx, dx, dy * dy);
-      if (d < dbest) {
-        dbest = d;
-        kbest = k;
-      }
-    }
-    a.out[n] = s_lab[kbest];
+    const float2* xp = a.x2 + b * (a.n_sym * 2) + 2 * nl;
+    const float2 y = wl_out(w, g, xp[1], xp[0], xp[-1], xp[-2]);
+    const int d = decide(y, a.lut, s_pts, a.m);
+    a.out[n] = s_lab[d];
     if (a.pattern) {
       int64_t pi = (a.n_off0 + n) % a.P;
       if (pi < 0) pi += a.P;
       const int ref = a.pattern[pi];
-      se = (ref != kbest) ? 1u : 0u;
-      be = __popc((unsigned)(s_lab[kbest] ^ s_lab[ref]));
+      se = (ref != d) ? 1u : 0u;
+      be = __popc((unsigned)(s_lab[d] ^ s_lab[ref]));
     }
   }
-  se = __reduce_add_sync(0xffffffffu, se);
-  be = __reduce_add_sync(0xffffffffu, be);
+  se = warp_sum(se);
+  be = warp_sum(be);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
     s_red[0][warp] = se;

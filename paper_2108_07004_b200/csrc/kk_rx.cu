@@ -42,29 +42,37 @@ struct kk_rx {
   int64_t x2h = 0;
   float dc = 0, vmin = 1, a_hat = 0, mu = 1e-3f, tau = 0;
   int mode = 0;
-  uint32_t tb_mod = 0, s32 = 0, s512 = 0;
+  uint32_t tb_mod = 0, s32 = 0;
   int64_t P = 0, ref_offset = 0, stream_index = 0;
   bool has_pattern = false;
   uint32_t dump = 0;
-  int grid_x2 = 0;
-  // device
+  int grid_chain = 0;
+  // constant tables
   float2 *d_tw = nullptr, *d_tw512 = nullptr, *d_H = nullptr, *d_pts = nullptr, *d_winit = nullptr;
+  unsigned long long* d_lut = nullptr;
+  DecLut lut{};
   uint8_t *d_lab = nullptr, *d_pattern = nullptr;
-  float2* d_x2buf = nullptr;  // x2 index -x2h .. max_batch*N/2
-  float2* d_taps = nullptr;
-  unsigned long long* d_counts = nullptr;
-  uint8_t* d_out = nullptr;
+  // per-chunk scratch (grown on demand to the largest chunk seen)
+  int64_t cap = 0;                       // buffers
+  float2* d_tails = nullptr;             // [cap + 1][x2h]  update-pass tails of x2
+  float2* d_taps = nullptr;              // [cap * nsub][8]
+  unsigned long long* d_counts = nullptr;  // [cap][8]
+  unsigned long long* h_counts = nullptr;  // pinned [cap][8]
+  uint8_t* d_out = nullptr;              // labels staging for host outputs [cap * n_sym]
+  // full x2 (sub_block < buffer or debug), max_batch buffers
+  float2* d_x2full = nullptr;            // x2 index -x2h .. max_batch*N/2
+  float2* d_es = nullptr;                // debug E_s [max_batch * N]
+  // host-input staging (double-buffered, max_batch buffers each)
   int16_t* d_stage[2] = {nullptr, nullptr};
-  float2* d_es = nullptr;
-  unsigned long long* h_counts = nullptr;  // pinned
   cudaStream_t stream = nullptr, copy_stream = nullptr;
   bool own_stream = false;
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   kk_rx_counts totals{};
   kk_status sticky = KK_OK;
-  int last_nb = 0;
+  int64_t last_nb = 0;
+  bool last_full = false;                // the last chunk materialised full x2
   int64_t last_launches = 0;
-  // per-kernel timing (kk_rx_set_timing): events around each kernel of a batch
+  // per-kernel timing (kk_rx_set_timing): events around each launch slot of a chunk
   bool timing = false;
   cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
   double kernel_ms[3] = {0, 0, 0};
@@ -97,6 +105,80 @@ static void halo_geometry(int64_t N, int K, int64_t* left, int64_t* right, int* 
   if (spb) *spb = steps;
   if (i0) *i0 = first;
   if (x2h) *x2h = X2H;
+}
+
+// Exact decision look-up table: a G x G grid over the
+// constellation's bounding box (+2 d_min).  For each cell R (enlarged by 1e-3 of a
+// cell to absorb fp32 index rounding) the candidate list holds every point k with
+//   min_{y in R} |y - p_k|^2  <=  min_j max_{y in R} |y - p_j|^2  (+ slack)
+// i.e. every point that can be nearest anywhere in R, in ascending index order, so
+// argmin over the list == brute-force argmin with the lowest-index tie rule.
+// Packed per cell: count in bits 60..63 (15 = brute force), 7-bit indices.
+static bool build_lut_g(const std::vector<double>& pts, int m, int G, DecLut& L, std::vector<unsigned long long>& cells,
+                        int* n_brute) {
+  double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300, dmin = 1e300;
+  for (int k = 0; k < m; ++k) {
+    xmin = std::min(xmin, pts[2 * k]);
+    xmax = std::max(xmax, pts[2 * k]);
+    ymin = std::min(ymin, pts[2 * k + 1]);
+    ymax = std::max(ymax, pts[2 * k + 1]);
+    for (int j = 0; j < k; ++j)
+      dmin = std::min(dmin, std::hypot(pts[2 * k] - pts[2 * j], pts[2 * k + 1] - pts[2 * j + 1]));
+  }
+  const double pad = 2.0 * dmin;
+  const double span = std::max(xmax - xmin, ymax - ymin) + 2 * pad;
+  const float x0 = (float)(xmin - pad), y0 = (float)(ymin - pad);
+  const float inv = (float)(G / span);
+  const double cs = 1.0 / (double)inv;
+  cells.assign((size_t)G * G, 0);
+  int nb = 0;
+  std::vector<double> mind(m);
+  for (int cy = 0; cy < G; ++cy)
+    for (int cx = 0; cx < G; ++cx) {
+      const double e = 1e-3 * cs;
+      const double xl = x0 + cx * cs - e, xh = x0 + (cx + 1) * cs + e;
+      const double yl = y0 + cy * cs - e, yh = y0 + (cy + 1) * cs + e;
+      double U = 1e300;
+      for (int k = 0; k < m; ++k) {
+        const double px = pts[2 * k], py = pts[2 * k + 1];
+        const double dx = std::max(0.0, std::max(xl - px, px - xh)), dy = std::max(0.0, std::max(yl - py, py - yh));
+        mind[k] = dx * dx + dy * dy;
+        const double fx = std::max(std::fabs(px - xl), std::fabs(px - xh)),
+                     fy = std::max(std::fabs(py - yl), std::fabs(py - yh));
+        U = std::min(U, fx * fx + fy * fy);
+      }
+      const double slack = 1e-5 * (1.0 + U);
+      unsigned long long w = 0;
+      int c = 0;
+      for (int k = 0; k < m && c <= 8; ++k)
+        if (mind[k] <= U + slack) {
+          if (c < 8) w |= (unsigned long long)k << (7 * c);
+          ++c;
+        }
+      if (c > 8) {
+        w = 15ull << 60;
+        ++nb;
+      } else {
+        w |= (unsigned long long)c << 60;
+      }
+      cells[(size_t)cy * G + cx] = w;
+    }
+  L.g = G;
+  L.x0 = x0;
+  L.y0 = y0;
+  L.inv = inv;
+  *n_brute = nb;
+  return true;
+}
+
+static void build_lut(const std::vector<double>& pts, int m, DecLut& L, std::vector<unsigned long long>& cells) {
+  L = DecLut{};
+  cells.clear();
+  if (m <= 8) return;  // brute force is as cheap as a lookup
+  // 64 x 64 cells (32 KB, L2/L1 resident): ~1-3 candidates per cell for M <= 128
+  int nb = 0;
+  build_lut_g(pts, m, 64, L, cells, &nb);
+  if (nb * 20 > 64 * 64) build_lut_g(pts, m, 128, L, cells, &nb);
 }
 
 extern "C" {
@@ -148,8 +230,9 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
-  void* ptrs[] = {h->d_tw, h->d_tw512, h->d_H, h->d_pts, h->d_winit, h->d_lab, h->d_pattern, h->d_x2buf,
-                  h->d_taps, h->d_counts, h->d_out, h->d_stage[0], h->d_stage[1], h->d_es};
+  void* ptrs[] = {h->d_tw,     h->d_tw512,  h->d_H,      h->d_pts,    h->d_winit,    h->d_lut,
+                  h->d_lab,    h->d_pattern, h->d_tails, h->d_taps,   h->d_counts,   h->d_out,
+                  h->d_x2full, h->d_es,     h->d_stage[0], h->d_stage[1]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_counts) cudaFreeHost(h->h_counts);
@@ -268,7 +351,6 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   if (tb < 0) tb += buffer_len;
   h->tb_mod = (uint32_t)tb;
   h->s32 = (uint32_t)((tb * 32) % buffer_len);
-  h->s512 = (uint32_t)((tb * 512) % buffer_len);
   h->has_pattern = p->ref_pattern != nullptr;
   h->P = h->has_pattern ? p->ref_len : 1;
   h->ref_offset = p->ref_offset;
@@ -286,15 +368,30 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
       const double a = -2.0 * M_PI * (double)(r * l) / 512.0;
       tw512[r * 32 + l] = make_float2((float)std::cos(a), (float)std::sin(a));
     }
-  for (int k = 0; k < 1024; ++k) {
-    std::complex<double> acc = 0;
+  // S4 with the downconversion moved behind the LTI filter:
+  //   x2[m] = e^{i theta_{2m}} sum_i h'_i D[2m - i],  h'_i = h_i e^{-2 pi i tb i / N}
+  // Hs = DFT_1024(h' placed circularly) / 1024, fp64, rounded once (reading R16).
+  {
+    int64_t tbn = p->tone_bin % buffer_len;
+    if (tbn < 0) tbn += buffer_len;
+    std::vector<std::complex<double>> hp(203);
     for (int t = 0; t < 203; ++t) {
-      const int i = t - 101;
-      const double a = -2.0 * M_PI * (double)(((int64_t)k * (i + 1024)) % 1024) / 1024.0;
-      acc += std::complex<double>(p->fir[2 * t], p->fir[2 * t + 1]) * std::complex<double>(std::cos(a), std::sin(a));
+      const int64_t i = t - 101;
+      int64_t ph = (tbn * i) % buffer_len;
+      if (ph < 0) ph += buffer_len;
+      const double a = -2.0 * M_PI * (double)ph / (double)buffer_len;
+      hp[t] = std::complex<double>(p->fir[2 * t], p->fir[2 * t + 1]) * std::complex<double>(std::cos(a), std::sin(a));
     }
-    acc /= 1024.0;
-    Hs[k] = make_float2((float)acc.real(), (float)acc.imag());
+    for (int k = 0; k < 1024; ++k) {
+      std::complex<double> acc = 0;
+      for (int t = 0; t < 203; ++t) {
+        const int i = t - 101;
+        const double a = -2.0 * M_PI * (double)(((int64_t)k * (i + 1024)) % 1024) / 1024.0;
+        acc += hp[t] * std::complex<double>(std::cos(a), std::sin(a));
+      }
+      acc /= 1024.0;
+      Hs[k] = make_float2((float)acc.real(), (float)acc.imag());
+    }
   }
   for (int k = 0; k < m; ++k) fpts[k] = make_float2((float)pts[2 * k], (float)pts[2 * k + 1]);
   if (p->w_init) {
@@ -338,11 +435,9 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   CKC(cudaMalloc(&h->d_winit, 8 * sizeof(float2)));
   CKC(cudaMalloc(&h->d_lab, 128));
   CKC(cudaMalloc(&h->d_pattern, (size_t)h->P));
-  CKC(cudaMalloc(&h->d_x2buf, (size_t)(h->x2h + (int64_t)B * h->N / 2) * sizeof(float2)));
-  CKC(cudaMalloc(&h->d_taps, (size_t)B * h->nsub * 8 * sizeof(float2)));
-  CKC(cudaMalloc(&h->d_counts, (size_t)B * 8 * sizeof(unsigned long long)));
-  CKC(cudaMalloc(&h->d_out, (size_t)B * h->n_sym));
-  CKC(cudaMallocHost(&h->h_counts, (size_t)B * 8 * sizeof(unsigned long long)));
+  if (h->nsub > 1 || (h->dump & (KK_DUMP_ES | KK_DUMP_X2))) {
+    CKC(cudaMalloc(&h->d_x2full, (size_t)(h->x2h + (int64_t)B * h->N / 2 + 64) * sizeof(float2)));
+  }
   if (h->dump & KK_DUMP_ES) CKC(cudaMalloc(&h->d_es, (size_t)B * h->N * sizeof(float2)));
   CKC(cudaMemcpy(h->d_tw, tw.data(), 1024 * sizeof(float2), cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(h->d_tw512, tw512.data(), 512 * sizeof(float2), cudaMemcpyHostToDevice));
@@ -351,7 +446,16 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   CKC(cudaMemcpy(h->d_winit, winit.data(), 8 * sizeof(float2), cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(h->d_lab, lab8.data(), m, cudaMemcpyHostToDevice));
   if (h->has_pattern) CKC(cudaMemcpy(h->d_pattern, p->ref_pattern, (size_t)h->P, cudaMemcpyHostToDevice));
-  h->grid_x2 = x2_occupancy_grid(dev);
+  {
+    std::vector<unsigned long long> cells;
+    build_lut(pts, m, h->lut, cells);
+    if (h->lut.g > 0) {
+      CKC(cudaMalloc(&h->d_lut, cells.size() * sizeof(unsigned long long)));
+      CKC(cudaMemcpy(h->d_lut, cells.data(), cells.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+      h->lut.cell = h->d_lut;
+    }
+  }
+  CKC(chain_setup(dev, &h->grid_chain));
   CKC(cudaGetLastError());
 #undef CKC
   *out = h;
@@ -381,81 +485,162 @@ static bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-static kk_status run_batch(kk_rx_t* h, const int16_t* codes_dev, int nb, int64_t stream_index) {
+static void fill_chain_common(kk_rx_t* h, ChainArgs& ca, const int16_t* codes_dev) {
+  ca.codes = codes_dev;
+  ca.N = h->N;
+  ca.x2h = h->x2h;
+  ca.dc = h->dc;
+  ca.vmin = h->vmin;
+  ca.a_hat = h->a_hat;
+  ca.invN = (float)(1.0 / (double)h->N);
+  ca.tb_mod = h->tb_mod;
+  ca.s32 = h->s32;
+  ca.tw1024 = h->d_tw;
+  ca.tw512 = h->d_tw512;
+  ca.Hs = h->d_H;
+  ca.aligned16 = ((uintptr_t)codes_dev % 16) == 0;
+  ca.n_sym = h->n_sym;
+  ca.m = h->m;
+  ca.pts = h->d_pts;
+  ca.labels = h->d_lab;
+  ca.pattern = h->has_pattern ? h->d_pattern : nullptr;
+  ca.P = h->P;
+  ca.lut = h->lut;
+}
+
+static int64_t seg_steps(const Seg& g) { return (int64_t)g.n_own * (g.i_end - g.i_begin); }
+
+static kk_status grow(kk_rx_t* h, int64_t nb) {
+  if (nb <= h->cap) return KK_OK;
+  void* olds[] = {h->d_tails, h->d_taps, h->d_counts, h->d_out};
+  for (void* p : olds)
+    if (p) cudaFree(p);
+  if (h->h_counts) cudaFreeHost(h->h_counts);
+  h->d_tails = nullptr;
+  h->d_taps = nullptr;
+  h->d_counts = nullptr;
+  h->d_out = nullptr;
+  h->h_counts = nullptr;
+  h->cap = 0;
+  CK(cudaMalloc(&h->d_tails, (size_t)((nb + 1) * h->x2h + 64) * sizeof(float2)));
+  CK(cudaMalloc(&h->d_taps, (size_t)nb * h->nsub * 8 * sizeof(float2)));
+  CK(cudaMalloc(&h->d_counts, (size_t)nb * 8 * sizeof(unsigned long long)));
+  CK(cudaMalloc(&h->d_out, (size_t)nb * h->n_sym));
+  CK(cudaMallocHost(&h->h_counts, (size_t)nb * 8 * sizeof(unsigned long long)));
+  h->cap = nb;
+  return KK_OK;
+}
+
+// Launch sequence of one chunk of nb buffers:
+//  sub_block == buffer (default):  [1] x2 update-pass tails  [2] LMS  [3] fused S1-S7
+//  sub_block <  buffer          :  [1] full x2               [2] LMS  [3] apply/decide/count
+//  KK_DUMP_*                     :  + a debug full-x2 pass (E_s / x2 for kk_rx_debug_*)
+// `out_dev`: where the labels go (the caller's device buffer, or d_out).
+static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int64_t stream_index, uint8_t* out_dev,
+                           bool full) {
   const int64_t Pp = h->P;
   int64_t n_off0 = h->has_pattern ? ((h->ref_offset + (stream_index % Pp) * (h->n_sym % Pp)) % Pp) : 0;
   if (n_off0 < 0) n_off0 += Pp;
   CK(cudaMemsetAsync(h->d_counts, 0, (size_t)nb * 8 * sizeof(unsigned long long), h->stream));
-  float2* x2 = h->d_x2buf + h->x2h;
-  X2Args xa{};
-  xa.codes = codes_dev;
-  xa.N = h->N;
-  xa.steps_per_buf = h->steps_per_buf;
-  xa.pre_first_step = h->pre_first;
-  xa.pre_steps = h->pre_steps;
-  xa.nbuf = nb;
-  xa.total_steps = (int64_t)h->pre_steps + (int64_t)nb * h->steps_per_buf;
-  xa.dc = h->dc;
-  xa.vmin = h->vmin;
-  xa.a_hat = h->a_hat;
-  xa.invN = (float)(1.0 / (double)h->N);
-  xa.tb_mod = h->tb_mod;
-  xa.s32 = h->s32;
-  xa.s512 = h->s512;
-  xa.x2 = x2;
-  xa.x2_lo = -h->x2h;
-  xa.tw1024 = h->d_tw;
-  xa.tw512 = h->d_tw512;
-  xa.H = h->d_H;
-  xa.counts = h->d_counts;
-  xa.es_dump = h->d_es;
-  xa.aligned16 = ((uintptr_t)codes_dev % 16) == 0;
+  const int S = h->steps_per_buf;
+  const bool fused = h->nsub == 1;
+  float2* x2f0 = h->d_x2full ? h->d_x2full + h->x2h : nullptr;  // x2 index 0 of buffer 0
+  auto full_pass = [&](int count_clip, float2* es) -> kk_status {
+    ChainArgs ca{};
+    fill_chain_common(h, ca, codes_dev);
+    ca.nseg = 2;
+    ca.seg[0] = Seg{-1, 1, h->pre_first, S, SEG_X2_FULL, 0, 0, 0, x2f0, nullptr, nullptr, nullptr, 0};
+    ca.seg[1] = Seg{0, (int32_t)nb, 0, S, SEG_X2_FULL, count_clip, 0, 0, x2f0, nullptr, h->d_counts, nullptr, 0};
+    ca.es_dump = es;
+    ca.total_steps = seg_steps(ca.seg[0]) + seg_steps(ca.seg[1]);
+    CK(launch_chain(ca, h->grid_chain, h->stream));
+    h->last_launches += 1;
+    return KK_OK;
+  };
   if (h->timing) CK(cudaEventRecord(h->ev_t[0], h->stream));
-  CK(launch_x2(xa, h->grid_x2, h->stream));
+  // [1] x2: update-pass tails of owners -1 .. nb-2 (chain b reads tail b), or everything
+  if (fused) {
+    ChainArgs ca{};
+    fill_chain_common(h, ca, codes_dev);
+    ca.nseg = 1;
+    ca.seg[0] = Seg{-1, (int32_t)nb, h->pre_first, S, SEG_X2_TAIL, 0, 0, 0, h->d_tails, nullptr, nullptr, nullptr, 0};
+    ca.total_steps = seg_steps(ca.seg[0]);
+    CK(launch_chain(ca, h->grid_chain, h->stream));
+    h->last_launches += 1;
+  } else {
+    kk_status st = full_pass(1, h->d_es);
+    if (st != KK_OK) return st;
+  }
   if (h->timing) CK(cudaEventRecord(h->ev_t[1], h->stream));
-  LmsArgs la{};
-  la.x2 = x2;
-  la.n_sym = h->n_sym;
-  la.L = h->L;
-  la.nsub = h->nsub;
-  la.nchains = nb * h->nsub;
-  la.K = h->K;
-  la.mu = h->mu;
-  la.tau = h->tau;
-  la.mode = h->mode;
-  la.m = h->m;
-  la.pts = h->d_pts;
-  la.pattern = h->has_pattern ? h->d_pattern : nullptr;
-  la.P = Pp;
-  la.n_off0 = n_off0;
-  la.w_init = h->d_winit;
-  la.taps = h->d_taps;
-  la.counts = h->d_counts;
-  CK(launch_lms(la, h->stream));
+  // [2] LMS update pass
+  {
+    LmsArgs la{};
+    if (fused) {
+      la.x2_b0 = h->d_tails + h->x2h;
+      la.x2_stride = h->x2h;
+    } else {
+      la.x2_b0 = x2f0;
+      la.x2_stride = h->N / 2;
+    }
+    la.n_sym = h->n_sym;
+    la.L = h->L;
+    la.nsub = h->nsub;
+    la.nchains = (int32_t)(nb * h->nsub);
+    la.K = h->K;
+    la.mu = h->mu;
+    la.inv_tau = h->tau > 0.f ? 1.0f / h->tau : 0.f;
+    la.mode = h->mode;
+    la.m = h->m;
+    la.pts = h->d_pts;
+    la.pattern = h->has_pattern ? h->d_pattern : nullptr;
+    la.P = Pp;
+    la.n_off0 = n_off0;
+    la.w_init = h->d_winit;
+    la.taps = h->d_taps;
+    la.counts = h->d_counts;
+    CK(launch_lms(la, h->stream));
+    h->last_launches += 1;
+  }
   if (h->timing) CK(cudaEventRecord(h->ev_t[2], h->stream));
-  ApplyArgs aa{};
-  aa.x2 = x2;
-  aa.n_sym = h->n_sym;
-  aa.L = h->L;
-  aa.nsub = h->nsub;
-  aa.total = (int64_t)nb * h->n_sym;
-  aa.m = h->m;
-  aa.pts = h->d_pts;
-  aa.labels = h->d_lab;
-  aa.pattern = h->has_pattern ? h->d_pattern : nullptr;
-  aa.P = Pp;
-  aa.n_off0 = n_off0;
-  aa.taps = h->d_taps;
-  aa.out = h->d_out;
-  aa.counts = h->d_counts;
-  CK(launch_apply(aa, h->stream));
+  // [3] fused chain (or apply from materialised x2)
+  if (fused) {
+    ChainArgs ca{};
+    fill_chain_common(h, ca, codes_dev);
+    ca.nseg = 1;
+    ca.seg[0] = Seg{0, (int32_t)nb, 0, S, SEG_APPLY, 1, 0, 0, nullptr, out_dev, h->d_counts, h->d_taps, n_off0};
+    ca.total_steps = seg_steps(ca.seg[0]);
+    CK(launch_chain(ca, h->grid_chain, h->stream));
+  } else {
+    ApplyArgs aa{};
+    aa.x2 = x2f0;
+    aa.n_sym = h->n_sym;
+    aa.L = h->L;
+    aa.nsub = h->nsub;
+    aa.total = nb * h->n_sym;
+    aa.m = h->m;
+    aa.pts = h->d_pts;
+    aa.labels = h->d_lab;
+    aa.pattern = h->has_pattern ? h->d_pattern : nullptr;
+    aa.P = Pp;
+    aa.n_off0 = n_off0;
+    aa.taps = h->d_taps;
+    aa.out = out_dev;
+    aa.counts = h->d_counts;
+    aa.lut = h->lut;
+    CK(launch_apply(aa, h->stream));
+  }
+  h->last_launches += 1;
   if (h->timing) CK(cudaEventRecord(h->ev_t[3], h->stream));
-  h->last_launches += 3;  // kk_x2, kk_lms, kk_apply
+  if (fused && full) {
+    kk_status st = full_pass(0, h->d_es);
+    if (st != KK_OK) return st;
+  }
+  h->last_full = full || !fused;
   return KK_OK;
 }
 
-static kk_status finish_counts(kk_rx_t* h, int nb, kk_rx_counts* out_per_buf) {
-  for (int b = 0; b < nb; ++b) {
+static kk_status finish_counts(kk_rx_t* h, int64_t nb, kk_rx_counts* out_per_buf) {
+  for (int64_t b = 0; b < nb; ++b) {
     const unsigned long long* c = h->h_counts + 8 * b;
     kk_rx_counts r{};
     r.bit_errors = c[C_BITERR];
@@ -492,32 +677,37 @@ kk_status kk_rx_process_batch(kk_rx_t* h, const int16_t* first, int64_t nbuf, ui
   h->last_launches = 0;
   const bool in_dev = is_device_ptr(first);
   const bool out_dev = out_symbols ? is_device_ptr(out_symbols) : false;
-  const int B = h->max_batch;
+  const bool full = (h->dump & (KK_DUMP_ES | KK_DUMP_X2)) != 0;
+  // chunking: device input on the fused path runs the whole call as one chunk
+  // (one LMS latency per call); host input, sub_block < buffer and debug dumps
+  // use chunks of max_batch buffers.
+  const int64_t B = (in_dev && h->nsub == 1 && !full) ? nbuf : std::min<int64_t>(h->max_batch, nbuf);
+  kk_status st = grow(h, B);
+  if (st != KK_OK) return st;
   const int64_t span_extra = h->left + h->right;
   if (!in_dev) {
     for (int i = 0; i < 2; ++i)
       if (!h->d_stage[i]) {
-        cudaError_t e = cudaMalloc(&h->d_stage[i], (size_t)(span_extra + (int64_t)B * h->N) * sizeof(int16_t));
+        cudaError_t e = cudaMalloc(&h->d_stage[i], (size_t)(span_extra + (int64_t)h->max_batch * h->N) * sizeof(int16_t));
         if (e != cudaSuccess) return fail(KK_ENOMEM, "staging allocation failed");
       }
   }
-  auto issue_h2d = [&](int64_t j0, int nb, int slot) -> kk_status {
+  auto issue_h2d = [&](int64_t j0, int64_t nb, int slot) -> kk_status {
     const int16_t* src = first + j0 * h->N - h->left;
-    const size_t bytes = (size_t)(span_extra + (int64_t)nb * h->N) * sizeof(int16_t);
+    const size_t bytes = (size_t)(span_extra + nb * h->N) * sizeof(int16_t);
     CK(cudaStreamWaitEvent(h->copy_stream, h->ev_used[slot], 0));
     CK(cudaMemcpyAsync(h->d_stage[slot], src, bytes, cudaMemcpyHostToDevice, h->copy_stream));
     CK(cudaEventRecord(h->ev_h2d[slot], h->copy_stream));
-    h->last_launches += 0;
     return KK_OK;
   };
   int64_t j0 = 0;
   int slot = 0;
   if (!in_dev) {
-    kk_status s = issue_h2d(0, (int)std::min<int64_t>(B, nbuf), 0);
-    if (s != KK_OK) return s;
+    st = issue_h2d(0, std::min<int64_t>(B, nbuf), 0);
+    if (st != KK_OK) return st;
   }
   while (j0 < nbuf) {
-    const int nb = (int)std::min<int64_t>(B, nbuf - j0);
+    const int64_t nb = std::min<int64_t>(B, nbuf - j0);
     const int16_t* codes;
     if (in_dev) {
       codes = first + j0 * h->N;
@@ -525,19 +715,20 @@ kk_status kk_rx_process_batch(kk_rx_t* h, const int16_t* first, int64_t nbuf, ui
       CK(cudaStreamWaitEvent(h->stream, h->ev_h2d[slot], 0));
       codes = h->d_stage[slot] + h->left;
     }
-    kk_status s = run_batch(h, codes, nb, h->stream_index + j0);
-    if (s != KK_OK) return s;
+    uint8_t* odev = (out_symbols && out_dev) ? out_symbols + j0 * h->n_sym : h->d_out;
+    st = run_chunk(h, codes, nb, h->stream_index + j0, odev, full);
+    if (st != KK_OK) return st;
     if (!in_dev) {
       CK(cudaEventRecord(h->ev_used[slot], h->stream));
       const int64_t jn = j0 + nb;
       if (jn < nbuf) {
-        s = issue_h2d(jn, (int)std::min<int64_t>(B, nbuf - jn), slot ^ 1);
-        if (s != KK_OK) return s;
+        st = issue_h2d(jn, std::min<int64_t>(B, nbuf - jn), slot ^ 1);
+        if (st != KK_OK) return st;
       }
     }
-    if (out_symbols) {
-      CK(cudaMemcpyAsync(out_symbols + j0 * h->n_sym, h->d_out, (size_t)nb * h->n_sym,
-                         out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+    if (out_symbols && !out_dev) {
+      CK(cudaMemcpyAsync(out_symbols + j0 * h->n_sym, h->d_out, (size_t)nb * h->n_sym, cudaMemcpyDeviceToHost,
+                         h->stream));
     }
     CK(cudaMemcpyAsync(h->h_counts, h->d_counts, (size_t)nb * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        h->stream));
@@ -585,17 +776,30 @@ kk_status kk_rx_reset_totals(kk_rx_t* h) {
 
 kk_status kk_rx_debug_x2(kk_rx_t* h, int64_t first, int64_t count, float* out) {
   if (!h || !out || count < 0) return fail(KK_EINVAL, "bad arguments");
-  if (first < -(2 * (int64_t)h->K + 2) || first + count > (int64_t)h->last_nb * h->N / 2)
+  if (first < -(2 * (int64_t)h->K + 2) || first + count > h->last_nb * h->N / 2)
     return fail(KK_EINVAL, "x2 range outside the last batch");
   CK(cudaSetDevice(h->device));
-  CK(cudaMemcpy(out, h->d_x2buf + h->x2h + first, (size_t)count * sizeof(float2), cudaMemcpyDeviceToHost));
+  if (h->last_full && h->d_x2full) {
+    CK(cudaMemcpy(out, h->d_x2full + h->x2h + first, (size_t)count * sizeof(float2), cudaMemcpyDeviceToHost));
+    return KK_OK;
+  }
+  // only the update-pass tails are materialised: [b*N/2 - x2h, b*N/2) for b in [0, nb)
+  std::vector<float2> tmp((size_t)count, make_float2(NAN, NAN));
+  for (int64_t b = 0; b < h->last_nb; ++b) {
+    const int64_t lo = b * h->N / 2 - h->x2h, hi = b * h->N / 2;
+    const int64_t a0 = std::max(lo, first), a1 = std::min(hi, first + count);
+    if (a1 > a0)
+      CK(cudaMemcpy(tmp.data() + (a0 - first), h->d_tails + b * h->x2h + (a0 - lo), (size_t)(a1 - a0) * sizeof(float2),
+                    cudaMemcpyDeviceToHost));
+  }
+  std::memcpy(out, tmp.data(), (size_t)count * sizeof(float2));
   return KK_OK;
 }
 
 kk_status kk_rx_debug_es(kk_rx_t* h, int64_t first, int64_t count, float* out) {
   if (!h || !out || count < 0) return fail(KK_EINVAL, "bad arguments");
   if (!h->d_es) return fail(KK_ESTATE, "create with debug_dump & KK_DUMP_ES");
-  if (first < 0 || first + count > (int64_t)h->last_nb * h->N) return fail(KK_EINVAL, "range outside the last batch");
+  if (first < 0 || first + count > h->last_nb * h->N) return fail(KK_EINVAL, "range outside the last batch");
   CK(cudaSetDevice(h->device));
   CK(cudaMemcpy(out, h->d_es + first, (size_t)count * sizeof(float2), cudaMemcpyDeviceToHost));
   return KK_OK;

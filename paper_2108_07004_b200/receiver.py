@@ -150,7 +150,7 @@ class KKReceiver:
         ms = (C.c_double * 3)()
         n = (C.c_int64 * 3)()
         check(self._lib.kk_rx_kernel_times(self.h, ms, n), "kk_rx_kernel_times")
-        return {k: (ms[i], n[i]) for i, k in enumerate(("kk_x2", "kk_lms", "kk_apply"))}
+        return {k: (ms[i], n[i]) for i, k in enumerate(("x2_pass", "lms", "chain"))}
 
     def close(self):
         if getattr(self, "h", None):

@@ -41,7 +41,7 @@ def _gpu_run(pool, cfg, fir, nbuf, first=0, dump=True, max_batch=None, host_inpu
     stream, off = make_stream(pool, nbuf, left, right, first=first)
     rx = KKReceiver(cfg.fmt if cfg.fmt.startswith("QAM") else "CUSTOM", cfg.buffer_len, cfg.cspr_db, fir,
                     pool.dc_offset, points=pool.points, labels=pool.labels, tone_bin=cfg.tbin,
-                    ref_pattern=pool.pattern, debug_dump=1 if dump else 0, max_batch=max_batch or nbuf, **kw)
+                    ref_pattern=pool.pattern, debug_dump=3 if dump else 0, max_batch=max_batch or nbuf, **kw)
     n_sym = cfg.buffer_len // 4
     if host_input:
         src = torch.from_numpy(stream).pin_memory()
@@ -169,9 +169,10 @@ def test_parity_update_variants(kw):
 
 
 def test_sharding_and_memory_kind_invariance():
-    """Outputs depend only on the raw window: a 4-buffer batch, 4 single-buffer
-    calls (max_batch=1), and host (pinned) input give bit-identical labels,
-    counters and taps (SURVEY 8(b) determinism; multi-GPU sharding relies on it)."""
+    """Outputs depend only on the raw window: one 4-buffer device call, host
+    (pinned) input in chunks of 1 and 3 buffers, and a single buffer processed
+    alone give bit-identical labels, counters and taps (SURVEY 8(b)
+    determinism; the multi-GPU buffer sharding relies on it)."""
     _require_gpu()
     name = "C2_n16"
     wl = configs.get(name)
@@ -179,16 +180,21 @@ def test_sharding_and_memory_kind_invariance():
     pool = make_pool(cfg, 4)
     fir = _fir(name)
     a = _gpu_run(pool, cfg, fir, 4, dump=False)
-    b = _gpu_run(pool, cfg, fir, 4, dump=False, max_batch=1)
+    b = _gpu_run(pool, cfg, fir, 4, dump=False, max_batch=1, host_input=True)
     c = _gpu_run(pool, cfg, fir, 4, dump=False, max_batch=3, host_input=True)
     assert np.array_equal(a["labels"], b["labels"]) and np.array_equal(a["labels"], c["labels"])
     assert a["counts"] == b["counts"] == c["counts"]
-    assert np.array_equal(a["rx"].taps(3), b["rx"].taps(0))
+    assert np.array_equal(a["rx"].taps(3), b["rx"].taps(0))   # b's last chunk = buffer 3
+    assert np.array_equal(a["rx"].taps(3), c["rx"].taps(0))   # c's last chunk = buffer 3
     # one buffer at stream position 2 alone == buffer 2 of the batch
     d = _gpu_run(pool, cfg, fir, 1, first=2, dump=False)
     n_sym = cfg.buffer_len // 4
     assert np.array_equal(d["labels"], a["labels"][2 * n_sym:3 * n_sym])
     assert d["counts"][0] == a["counts"][2]
+    assert np.array_equal(d["rx"].taps(0), a["rx"].taps(2))
+    # debug dumps (extra x2 pass) do not change the outputs
+    e = _gpu_run(pool, cfg, fir, 4, dump=True)
+    assert np.array_equal(a["labels"], e["labels"]) and a["counts"] == e["counts"]
 
 
 def test_full_size_c1_noiseless():
