@@ -117,29 +117,28 @@ __device__ __forceinline__ void bfly(float2& a, float2& b, int m) {
   }
 }
 
-// Forward DFT of length N (N in {16, 32}) over the register index, natural order:
-//   v[k] <- sum_n v[n] exp(-2 pi i n k / N)
-// radix-2 decimation in time; the input bit-reversal is a compile-time renaming.
+// Forward DFT of length N (N in {16, 32}) over the register index, radix-2
+// decimation in time, in place on BIT-REVERSED input storage:
+//   on entry v[brev(n)] holds x[n]; on exit v[k] holds X[k] = sum_n x[n] e^{-2 pi i n k / N}.
+// (DIT wants t[k] = x[brev(k)]; with that storage t is v itself, so no register
+// permutation is ever materialised.  Producers write their data bit-reversed for free.)
 template <int N>
-__device__ __forceinline__ void dft_reg(float2 (&v)[N]) {
+__device__ __forceinline__ void dft_brin(float2 (&v)[N]) {
   constexpr int LOGN = (N == 16) ? 4 : 5;
-  float2 t[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) t[k] = v[brev(k, LOGN)];
 #pragma unroll
   for (int st = 0; st < LOGN; ++st) {
     const int half = 1 << st;  // butterfly span
 #pragma unroll
     for (int start = 0; start < N; start += 2 * half) {
 #pragma unroll
-      for (int j = 0; j < half; ++j) bfly(t[start + j], t[start + j + half], j * (32 / (2 * half)));
+      for (int j = 0; j < half; ++j) bfly(v[start + j], v[start + j + half], j * (32 / (2 * half)));
     }
   }
-#pragma unroll
-  for (int k = 0; k < N; ++k) v[k] = t[k];
 }
 
-// Forward 1024-point DFT of one warp, lane layout in and out:
+// Forward 1024-point DFT of one warp:
+//   in : x[lane + 32 n2] at v[brev5(n2)]  (lane layout, registers bit-reversed)
+//   out: X[lane + 32 k2] at v[k2]          (lane layout, natural)
 //   X[k] = sum_n x[n] e^{-2 pi i n k / 1024}
 // scr: this warp's 32 x 33 float tile; tw: shared table tw[r*32 + l] = e^{-2 pi i r l / 1024}.
 // One copy of the 32-point DFT: the two passes are a loop.
@@ -147,7 +146,7 @@ __device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __rest
                                         const float2* __restrict__ tw) {
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
-    dft_reg<32>(v);
+    dft_brin<32>(v);
     if (pass == 0) {
 #pragma unroll
       for (int r = 1; r < 32; ++r) v[r] = c_mul(v[r], tw[r * 32 + lane]);
@@ -155,20 +154,20 @@ __device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __rest
       for (int r = 0; r < 32; ++r) scr[r * 33 + lane] = v[r].x;
       __syncwarp();
 #pragma unroll
-      for (int n = 0; n < 32; ++n) v[n].x = scr[lane * 33 + n];
+      for (int n = 0; n < 32; ++n) v[brev(n, 5)].x = scr[lane * 33 + n];
       __syncwarp();
 #pragma unroll
       for (int r = 0; r < 32; ++r) scr[r * 33 + lane] = v[r].y;
       __syncwarp();
 #pragma unroll
-      for (int n = 0; n < 32; ++n) v[n].y = scr[lane * 33 + n];
+      for (int n = 0; n < 32; ++n) v[brev(n, 5)].y = scr[lane * 33 + n];
       __syncwarp();
     }
   }
 }
 
 // Forward 512-point DFT of the folded spectrum, one warp:
-//   in : z[k2] = Z[lane + 32*k2], k2 in [0,16)
+//   in : Z[lane + 32*k2] at z[brev4(k2)], k2 in [0,16)   (registers bit-reversed)
 //   out: lane (2*r1 + h) gets z[r2] = X[r1 + 16*(r2 + 16*h)],  X[r] = sum_k Z[k] e^{-2 pi i k r / 512}
 // scr: this warp's tile (>= 16 x 34 floats); tw512[r1*32 + l] = e^{-2 pi i r1 l / 512} (global, L1).
 // The inverse transform the method needs is conj(DFT(conj(Z))), done by the caller.
@@ -177,7 +176,7 @@ __device__ __forceinline__ void fft512_pairs(float2 (&z)[16], int lane, float* _
   const int h = lane & 1, r1 = lane >> 1;
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
-    dft_reg<16>(z);
+    dft_brin<16>(z);
     if (pass == 0) {
 #pragma unroll
       for (int r = 1; r < 16; ++r) z[r] = c_mul(z[r], __ldg(tw512 + r * 32 + lane));
@@ -185,13 +184,13 @@ __device__ __forceinline__ void fft512_pairs(float2 (&z)[16], int lane, float* _
       for (int r = 0; r < 16; ++r) scr[r * 34 + lane] = z[r].x;
       __syncwarp();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) z[j].x = scr[r1 * 34 + 2 * j + h];
+      for (int j = 0; j < 16; ++j) z[brev(j, 4)].x = scr[r1 * 34 + 2 * j + h];
       __syncwarp();
 #pragma unroll
       for (int r = 0; r < 16; ++r) scr[r * 34 + lane] = z[r].y;
       __syncwarp();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) z[j].y = scr[r1 * 34 + 2 * j + h];
+      for (int j = 0; j < 16; ++j) z[brev(j, 4)].y = scr[r1 * 34 + 2 * j + h];
       __syncwarp();
     }
   }

@@ -25,10 +25,10 @@ constexpr int MAX_SEG = 4;
 enum SegMode { SEG_APPLY = 0, SEG_X2_TAIL = 1, SEG_X2_FULL = 2 };
 
 // exact decision look-up table (built on the host):
-// cell word = count (bits 60..63, 15 = brute force) | up to 8 ascending 7-bit
-// point indices (bits 7c .. 7c+6)
+// cell word = 4 ascending 7-bit point indices (bits 7c .. 7c+6; short lists are
+// padded with their first index) | bit 31 = brute force (crowded cell)
 struct DecLut {
-  const unsigned long long* cell;  // [g*g]
+  const uint32_t* cell;            // [g*g]
   float x0, y0, inv;               // cell (cx, cy) covers [x0 + cx/inv, ...)
   int g;                           // grid size (0 = no LUT: always brute force)
 };

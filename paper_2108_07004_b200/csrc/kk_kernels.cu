@@ -51,9 +51,9 @@ __device__ __forceinline__ void cis_turns(float t, float* s, float* c) {
 // Exact minimum-distance decision (ties -> lowest index, reading R11): the LUT
 // cell lists (ascending) every point that can be nearest anywhere in the
 // (slightly enlarged) cell; brute force outside the grid or for crowded cells.
-constexpr unsigned long long LUT_BRUTE = 15ull << 60;
+constexpr uint32_t LUT_BRUTE = 1u << 31;
 
-__device__ __forceinline__ unsigned long long lut_word(float2 y, const DecLut& L) {
+__device__ __forceinline__ uint32_t lut_word(float2 y, const DecLut& L) {
   if (L.g > 0) {
     const float fx = (y.x - L.x0) * L.inv, fy = (y.y - L.y0) * L.inv;
     if (fx >= 0.f && fy >= 0.f && fx < (float)L.g && fy < (float)L.g)
@@ -62,20 +62,36 @@ __device__ __forceinline__ unsigned long long lut_word(float2 y, const DecLut& L
   return LUT_BRUTE;
 }
 
-__device__ __forceinline__ int decide_word(float2 y, unsigned long long w, const float2* __restrict__ sp, int m) {
-  const int cnt = (int)(w >> 60);
-  const bool brute = cnt == 15;
-  const int n = brute ? m : cnt;
+__device__ __noinline__ int decide_brute(float2 y, const float2* __restrict__ sp, int m) {
   float best = __int_as_float(0x7f800000);
   int kb = 0;
-  for (int c = 0; c < n; ++c) {
-    const int k = brute ? c : (int)((w >> (7 * c)) & 127ull);
+  for (int k = 0; k < m; ++k) {
     const float dx = y.x - sp[k].x, dy = y.y - sp[k].y;
     const float d = fmaf(dx, dx, dy * dy);
     if (d < best) {
       best = d;
       kb = k;
     }
+  }
+  return kb;
+}
+
+// 4 candidates, branch-free (ascending order + strict < = lowest index on ties;
+// padded duplicates never replace); crowded / off-grid -> brute force (rare)
+__device__ __forceinline__ int decide_word(float2 y, uint32_t w, const float2* __restrict__ sp, int m) {
+  if (w & LUT_BRUTE) return decide_brute(y, sp, m);
+  int kb = (int)(w & 127u);
+  float dx = y.x - sp[kb].x, dy = y.y - sp[kb].y;
+  float best = fmaf(dx, dx, dy * dy);
+#pragma unroll
+  for (int c = 1; c < 4; ++c) {
+    const int k = (int)((w >> (7 * c)) & 127u);
+    dx = y.x - sp[k].x;
+    dy = y.y - sp[k].y;
+    const float d = fmaf(dx, dx, dy * dy);
+    const bool better = d < best;
+    best = better ? d : best;
+    kb = better ? k : kb;
   }
   return kb;
 }
@@ -209,10 +225,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
 
   // tone phase indices (tb * P) mod N of the EQ outputs: P = sbase + 768 q + 2 (r1 + 256 h) + 32 r2
   const uint32_t s3072 = tone_index(a, STEP);
-  uint32_t q_tap[NWARPS];
-#pragma unroll
-  for (int k = 0; k < NWARPS; ++k) q_tap[k] = tone_index(a, (int64_t)EQ_KEEP * k);
-  const uint32_t q_lane = tone_index(a, 2 * ((lane >> 1) + 256 * (lane & 1)));
+  // this warp's EQ block q = warp and lane offset 2 (r1 + 256 h), folded into one constant
+  const uint32_t q_lane = tone_index(a, (int64_t)EQ_KEEP * warp + 2 * ((lane >> 1) + 256 * (lane & 1)));
   uint32_t q_step = 0;
 
   StepPos cur = (g0 < g1) ? decode_step(a, g0) : StepPos{0, 0, 0};
@@ -290,12 +304,12 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
           for (int j = 0; j < 48; ++j) {
             const float vv = fmaxf((float)src[re0 + lane + 32 * j] + a.dc, a.vmin);
             const float l = __log2f(vv * invd) * 0.34657359027997264f;  // 0.5 * ln 2
-            if (j < 32) v[j].x = l;
-            if (j >= 16) v[j - 16].y = l;
+            if (j < 32) v[brev(j, 5)].x = l;        // FFT input registers are bit-reversed
+            if (j >= 16) v[brev(j - 16, 5)].y = l;
           }
         } else {
 #pragma unroll
-          for (int r = 0; r < 32; ++r) v[r] = ebuf[EQ_KEEP * warp + lane + 32 * r];
+          for (int r = 0; r < 32; ++r) v[brev(r, 5)] = ebuf[EQ_KEEP * warp + lane + 32 * r];
         }
         // transpose tile: H tasks use their own (not yet written) output slice of ebuf,
         // the warm-up task a slice of xs; E tasks reuse ebuf once every window is loaded.
@@ -309,13 +323,16 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
             // S2: phi = -H{l} <-> +i sgn(k) L_k (reading R1), /1024, conjugated so the
             // next forward FFT computes the inverse: IFFT(Y) = conj(FFT(conj(Y)))
             const float sc = 1.0f / 1024.0f;
+            float2 nv[32];
 #pragma unroll
             for (int k2 = 0; k2 < 32; ++k2) {
               const float2 y = v[k2];
               float2 r = (k2 < 16) ? make_float2(-y.y * sc, -y.x * sc) : make_float2(y.y * sc, y.x * sc);
               if ((k2 == 0 || k2 == 16) && lane == 0) r = make_float2(0.f, 0.f);
-              v[k2] = r;
+              nv[brev(k2, 5)] = r;  // bit-reversed input of the next transform
             }
+#pragma unroll
+            for (int k2 = 0; k2 < 32; ++k2) v[k2] = nv[k2];
           }
         }
         if (isH) {
@@ -378,7 +395,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
           for (int k2 = 0; k2 < 16; ++k2) {
             const float2 s0 = c_mul(v[k2], __ldg(a.Hs + lane + 32 * k2));
             const float2 s1 = c_mul(v[k2 + 16], __ldg(a.Hs + lane + 32 * (k2 + 16)));
-            z[k2] = make_float2(s0.x + s1.x, -(s0.y + s1.y));  // conj -> forward DFT = inverse
+            z[brev(k2, 4)] = make_float2(s0.x + s1.x, -(s0.y + s1.y));  // conj -> forward DFT = inverse
           }
           fft512_pairs(z, lane, scr, a.tw512);
           const int h = lane & 1, r1 = lane >> 1;
@@ -410,7 +427,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
             hi2 = (int)(h2 < hi2 ? (h2 > 0 ? h2 : 0) : hi2);
             dptr = sg.x2dst + dbase + (P0 >> 1);
           }
-          uint32_t qi = add_mod(add_mod(q_step, q_tap[q], n32), q_lane, n32);  // (tb * P0) mod N
+          uint32_t qi = add_mod(q_step, q_lane, n32);  // (tb * P0) mod N
 #pragma unroll
           for (int r2 = 0; r2 < 16; ++r2) {
             if (r2 >= lo2 && r2 < hi2) {
@@ -437,40 +454,43 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
       }
       uint8_t* outp = sg.out + ko * a.n_sym;
       constexpr int SPT = SYM_PER_STEP / (NWARPS * 32);  // symbols per thread per step (6)
-      constexpr int SB = 2;                               // symbols per inner batch
-#pragma unroll 1
-      for (int k0 = 0; k0 < SPT; k0 += SB) {
-        float2 yv[SB];
-        unsigned long long cw[SB];
+      int refv[SPT];
+      if (a.pattern) {
+        // pattern bytes first: these L2 loads are in flight while y and the LUT words are formed
 #pragma unroll
-        for (int k = 0; k < SB; ++k) {
-          // y = w^T u + g^T u* with u = (xs[2s+3], xs[2s+2], xs[2s+1], xs[2s]), factored taps
-          const int sidx = threadIdx.x + NWARPS * 32 * (k0 + k);
-          const float2 u[4] = {xs[2 * sidx + 3], xs[2 * sidx + 2], xs[2 * sidx + 1], xs[2 * sidx]};
-          float2 y = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            y.x = fmaf(ta[t].x, u[t].x, fmaf(ta[t].y, u[t].y, y.x));
-            y.y = fmaf(tc[t].x, u[t].x, fmaf(tc[t].y, u[t].y, y.y));
-          }
-          yv[k] = y;
-          cw[k] = lut_word(y, a.lut);  // independent loads, issued back to back
+        for (int k = 0; k < SPT; ++k) {
+          int64_t pi = pb + threadIdx.x + NWARPS * 32 * k;
+          while (pi >= a.P) pi -= a.P;
+          refv[k] = a.pattern[pi];
         }
+      }
+      float2 yv[SPT];
+      uint32_t cw[SPT];
 #pragma unroll
-        for (int k = 0; k < SB; ++k) {
-          const int sidx = threadIdx.x + NWARPS * 32 * (k0 + k);
-          const int64_t n = nbase + sidx;
-          if (n >= 0 && n < a.n_sym) {
-            const int d = decide_word(yv[k], cw[k], s_pts, a.m);
-            const uint8_t ld = s_lab[d];
-            outp[n] = ld;
-            if (a.pattern) {
-              int64_t pi = pb + sidx;
-              while (pi >= a.P) pi -= a.P;
-              const int ref = a.pattern[pi];
-              acc_se += (ref != d) ? 1u : 0u;
-              acc_be += __popc((unsigned)(ld ^ s_lab[ref]));
-            }
+      for (int k = 0; k < SPT; ++k) {
+        // y = w^T u + g^T u* with u = (xs[2s+3], xs[2s+2], xs[2s+1], xs[2s]), factored taps
+        const int sidx = threadIdx.x + NWARPS * 32 * k;
+        const float2 u[4] = {xs[2 * sidx + 3], xs[2 * sidx + 2], xs[2 * sidx + 1], xs[2 * sidx]};
+        float2 y = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          y.x = fmaf(ta[t].x, u[t].x, fmaf(ta[t].y, u[t].y, y.x));
+          y.y = fmaf(tc[t].x, u[t].x, fmaf(tc[t].y, u[t].y, y.y));
+        }
+        yv[k] = y;
+        cw[k] = lut_word(y, a.lut);
+      }
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        const int sidx = threadIdx.x + NWARPS * 32 * k;
+        const int64_t n = nbase + sidx;
+        if (n >= 0 && n < a.n_sym) {
+          const int d = decide_word(yv[k], cw[k], s_pts, a.m);
+          const uint8_t ld = s_lab[d];
+          outp[n] = ld;
+          if (a.pattern) {
+            acc_se += (refv[k] != d) ? 1u : 0u;
+            acc_be += __popc((unsigned)(ld ^ s_lab[refv[k]]));
           }
         }
       }

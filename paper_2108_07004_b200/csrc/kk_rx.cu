@@ -49,7 +49,7 @@ struct kk_rx {
   int grid_chain = 0;
   // constant tables
   float2 *d_tw = nullptr, *d_tw512 = nullptr, *d_H = nullptr, *d_pts = nullptr, *d_winit = nullptr;
-  unsigned long long* d_lut = nullptr;
+  uint32_t* d_lut = nullptr;
   DecLut lut{};
   uint8_t *d_lab = nullptr, *d_pattern = nullptr;
   // per-chunk scratch (grown on demand to the largest chunk seen)
@@ -114,7 +114,7 @@ static void halo_geometry(int64_t N, int K, int64_t* left, int64_t* right, int* 
 // i.e. every point that can be nearest anywhere in R, in ascending index order, so
 // argmin over the list == brute-force argmin with the lowest-index tie rule.
 // Packed per cell: count in bits 60..63 (15 = brute force), 7-bit indices.
-static bool build_lut_g(const std::vector<double>& pts, int m, int G, DecLut& L, std::vector<unsigned long long>& cells,
+static bool build_lut_g(const std::vector<double>& pts, int m, int G, DecLut& L, std::vector<uint32_t>& cells,
                         int* n_brute) {
   double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300, dmin = 1e300;
   for (int k = 0; k < m; ++k) {
@@ -148,18 +148,19 @@ static bool build_lut_g(const std::vector<double>& pts, int m, int G, DecLut& L,
         U = std::min(U, fx * fx + fy * fy);
       }
       const double slack = 1e-5 * (1.0 + U);
-      unsigned long long w = 0;
-      int c = 0;
-      for (int k = 0; k < m && c <= 8; ++k)
+      uint32_t w = 0;
+      int c = 0, first = -1;
+      for (int k = 0; k < m && c <= 4; ++k)
         if (mind[k] <= U + slack) {
-          if (c < 8) w |= (unsigned long long)k << (7 * c);
+          if (first < 0) first = k;
+          if (c < 4) w |= (uint32_t)k << (7 * c);
           ++c;
         }
-      if (c > 8) {
-        w = 15ull << 60;
+      if (c > 4 || c == 0) {
+        w = 1u << 31;  // brute force
         ++nb;
       } else {
-        w |= (unsigned long long)c << 60;
+        for (int q = c; q < 4; ++q) w |= (uint32_t)first << (7 * q);  // pad: duplicates never win a strict <
       }
       cells[(size_t)cy * G + cx] = w;
     }
@@ -171,14 +172,18 @@ static bool build_lut_g(const std::vector<double>& pts, int m, int G, DecLut& L,
   return true;
 }
 
-static void build_lut(const std::vector<double>& pts, int m, DecLut& L, std::vector<unsigned long long>& cells) {
+static void build_lut(const std::vector<double>& pts, int m, DecLut& L, std::vector<uint32_t>& cells) {
   L = DecLut{};
   cells.clear();
   if (m <= 8) return;  // brute force is as cheap as a lookup
-  // 64 x 64 cells (32 KB, L2/L1 resident): ~1-3 candidates per cell for M <= 128
+  // 64 x 64 cells (16 KB, L2/L1 resident): 1-4 candidates per cell for all built-in / GS formats
   int nb = 0;
   build_lut_g(pts, m, 64, L, cells, &nb);
-  if (nb * 20 > 64 * 64) build_lut_g(pts, m, 128, L, cells, &nb);
+  if (nb * 200 > 64 * 64) build_lut_g(pts, m, 128, L, cells, &nb);
+  if (nb * 200 > 128 * 128) {
+    L = DecLut{};  // too crowded for 4-candidate cells: brute force everywhere
+    cells.clear();
+  }
 }
 
 extern "C" {
@@ -447,11 +452,11 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   CKC(cudaMemcpy(h->d_lab, lab8.data(), m, cudaMemcpyHostToDevice));
   if (h->has_pattern) CKC(cudaMemcpy(h->d_pattern, p->ref_pattern, (size_t)h->P, cudaMemcpyHostToDevice));
   {
-    std::vector<unsigned long long> cells;
+    std::vector<uint32_t> cells;
     build_lut(pts, m, h->lut, cells);
     if (h->lut.g > 0) {
-      CKC(cudaMalloc(&h->d_lut, cells.size() * sizeof(unsigned long long)));
-      CKC(cudaMemcpy(h->d_lut, cells.data(), cells.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+      CKC(cudaMalloc(&h->d_lut, cells.size() * sizeof(uint32_t)));
+      CKC(cudaMemcpy(h->d_lut, cells.data(), cells.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
       h->lut.cell = h->d_lut;
     }
   }
