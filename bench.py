@@ -52,50 +52,63 @@ def _env_int(k, d):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """nvidia-smi clocks / throttle reasons streamed every 20 ms during the timed region
+    (B200_PROFILING.md "clocks DURING the timed region")."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.proc = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the first samples arrive before the timed region starts
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=10)
+        if self.proc is None:
+            return
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in (out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                self.samples.append(f)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(s[0]) for s in self.samples if num(s[0]) is not None]
+        smax = [num(s[1]) for s in self.samples if num(s[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for s in self.samples:
-            for n, v in zip(names, s[4:8]):
+            for n, v in zip(names, s[3:7]):
                 if v.strip().lower() in ("active", "1"):
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+        # only the samples taken under load (the sampler starts 0.3 s before the timed region)
+        load = sorted(sm)[len(sm) // 4:] if len(sm) > 4 else sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(smax) if smax else None,
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
@@ -158,7 +171,7 @@ def run_reference(args):
     rank = _env_int("RANK", 0)
     if rank != 0:
         return 0
-    workers = min(os.cpu_count() or 1, args.ref_workers)
+    workers = args.ref_workers or (os.cpu_count() or 1)
     from synth import configs
     from synth.generate import make_pool
     make_pool(configs.get(args.workload).link, args.pool)  # warm the input cache outside the timed steps
@@ -331,7 +344,9 @@ def run_gpu(args):
         "fp32_fraction_chain": value * FLOP_PER_SA_CHAIN / (FP32_PEAK_TFLOPS * 1e3),
         "roofline": {"bound": "alu", "kernel": "kk_chain_kernel<APPLY>", "achieved": achieved_tf,
                      "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tf / FP32_PEAK_TFLOPS,
-                     "traffic": (traffic or {}).get("chain_dram_bytes_per_launch") if traffic else None,
+                     "traffic": (traffic["chain_dram_bytes_per_launch"] * (B * N) / traffic["chain_samples_per_launch"]
+                                 if traffic else None),
+                     "traffic_source": (traffic or {}).get("source"),
                      "flop_per_sa": FLOP_PER_SA_KERNEL, "samples_per_launch": B * N, "avg_launch_ms": ch_avg_ms,
                      "hbm_algorithmic_bytes_per_launch": HBM_BYTES_PER_SA * B * N,
                      "hbm_achieved_gbs": HBM_BYTES_PER_SA * B * N / (ch_avg_ms / 1e3) / 1e9,
@@ -344,7 +359,7 @@ def run_gpu(args):
     if e2e:
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu_baseline:
-        workers = min(os.cpu_count() or 1, args.ref_workers)
+        workers = args.ref_workers or (os.cpu_count() or 1)
         v, dt, s = oracle_rate(args.workload, P, workers, workers)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": workers, "kind": "oracle",
                                 "sample": f"{workers} whole 2^22-sample C5 buffers, one per process ({dt:.1f} s)"}
@@ -358,13 +373,13 @@ def run_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kk", choices=["kk", "reference"])
     ap.add_argument("--workload", default="C5")
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--pool", type=int, default=16)
-    ap.add_argument("--ref-workers", type=int, default=8)
+    ap.add_argument("--ref-workers", type=int, default=0, help="oracle processes (0 = all host cores)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -1,0 +1,13 @@
+# Full evidence run (under gpurun): bench (with e2e + cpu_baseline), reference arm,
+# ncu launch list of the bench command, ncu --set full of the main chain launch.
+mkdir -p gpurun_out
+nvidia-smi > gpurun_out/nvsmi.txt 2>&1
+lscpu > gpurun_out/lscpu.txt 2>&1
+timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_full.log
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
+CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
+$CMD > gpurun_out/bench_short.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
+echo "launches rc=$?" >> gpurun_out/ncu_launches.log
+ncu --set full --clock-control none --import-source on -k regex:kk_chain -s 7 -c 1 -o gpurun_out/prof_bench_chain $CMD > gpurun_out/ncu_full.log 2>&1
+echo "full rc=$?" >> gpurun_out/ncu_full.log
