@@ -164,6 +164,20 @@ kk_status kk_rx_debug_es(kk_rx_t *h, int64_t first, int64_t count, float *out);
 /* Built-in constellation table (host only): 2*m floats, m labels. Returns m or <0. */
 int kk_rx_constellation(int fmt, float *points_out, uint8_t *labels_out);
 
+/* Host-only (tests): the two exact decision look-up tables the kernels use, built
+ * for `points` (2*m floats, re/im) and soft-gate `tau` (0 = hard / PILOT).
+ * lms_cells: 2*G*G floats (G = return value, 128): per cell (row-major, cell
+ * (cx,cy) at cy*G+cx) either the coordinates of the unique point that is nearest
+ * everywhere in the cell with every other point >= tau farther (FAST), or
+ * (NaN, bits of a word of 4 ascending 8-bit candidate indices, 128 = none;
+ * 0xffffffff = brute force) (SLOW).  Cell of y: floor(clamp(y*linv + lc, 0, G-1)),
+ * lms_geom = (lcx, lcy, linv).  dec_cells: g*g words of the fused chain's decision
+ * table (4 ascending 7-bit candidates, bit 31 = brute force), g <= 128;
+ * dec_geom = (x0, y0, inv, g), g = 0 when m <= 8 (brute force only).  Any output
+ * may be NULL.  Returns G, or -1 (bad arguments). */
+int kk_rx_decision_tables(const float *points, int m, float tau, float *lms_cells, float *lms_geom,
+                          uint32_t *dec_cells, float *dec_geom);
+
 /* Number of kernel launches issued by the last process call (for the bench). */
 int64_t kk_rx_last_launches(const kk_rx_t *h);
 

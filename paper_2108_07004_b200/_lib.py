@@ -74,6 +74,8 @@ EXPORTS = {
     "kk_rx_debug_es": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_float)]),
     "kk_rx_constellation": (C.c_int, [C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_uint8)]),
     "kk_rx_last_launches": (C.c_int64, [C.c_void_p]),
+    "kk_rx_decision_tables": (C.c_int, [C.POINTER(C.c_float), C.c_int, C.c_float, C.POINTER(C.c_float),
+                                        C.POINTER(C.c_float), C.POINTER(C.c_uint32), C.POINTER(C.c_float)]),
     "kk_rx_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "kk_rx_kernel_times": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "kk_rx_last_error": (C.c_char_p, [C.c_void_p]),

@@ -71,7 +71,22 @@ struct ChainArgs {
   DecLut lut;
 };
 
+// LMS update-pass look-up table (built on the host):
+// G x G cells (G a power of two) over the constellation's bounding box (+2 d_min).
+// Entry of cell (cx, cy) = float2:
+//   (px, py)          FAST: one point k is the nearest everywhere in the cell AND
+//                     every other point is >= tau farther (soft gate = 1): ref = p_k
+//   (NaN, bits(word)) SLOW: word = 4 ascending 8-bit point indices (128 = none)
+//                     holding every point that can be nearest or within tau of the
+//                     nearest anywhere in the cell; word = ~0u: brute force
+// The outermost ring of cells is always SLOW/brute (y is clamped into the grid).
+constexpr int LMS_LUT_G = 128;
+constexpr uint32_t LMS_BRUTE = 0xffffffffu;
+
+
 struct LmsArgs {
+  const float2* lut;       // [G*G] entries
+  float lcx, lcy, linv;    // cell coordinate = y * linv + lc (clamped to [0, G-1])
   const float2* x2_b0;     // x2 index 0 (position 0) of chain buffer 0
   int64_t x2_stride;       // x2 samples between consecutive buffers' position 0
   int64_t n_sym;           // symbols per buffer
@@ -112,6 +127,7 @@ enum { C_BITERR = 0, C_SYMERR = 1, C_BITS = 2, C_SYMS = 3, C_CLIP = 4, C_GATED =
 
 size_t chain_smem_bytes();
 cudaError_t chain_setup(int device, int* grid_out);
+cudaError_t lms_setup();
 cudaError_t launch_chain(const ChainArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_lms(const LmsArgs& a, cudaStream_t s);
 cudaError_t launch_apply(const ApplyArgs& a, cudaStream_t s);

@@ -525,9 +525,10 @@ cudaError_t launch_chain(const ChainArgs& a, int grid, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// Kernel 2: LMS update pass, one warp per sub-block chain (reading R10).
-// The chain is inherently sequential, so the kernel minimises the
-// per-step latency and instruction count:
+// Kernel 2: LMS update pass, one warp per sub-block chain (reading R10), 4 chains
+// per CTA sharing one LMS look-up table in shared memory.  The chain is
+// inherently sequential, so the kernel minimises the per-step
+// latency: the critical path is y_n -> decision -> e_n -> y_{n+1}.
 //  * the widely-linear filter y = w^T u + g^T u* is the real 2x2 matrix filter
 //      [y.x; y.y] = sum_k [[A_k, B_k], [C_k, D_k]] [u_k.x; u_k.y],
 //    A = w.x + g.x, B = g.y - w.y, C = w.y + g.y, D = w.x - g.x, and the LMS update
@@ -535,28 +536,79 @@ cudaError_t launch_chain(const ChainArgs& a, int grid, cudaStream_t s) {
 //    (16 FFMA per step instead of 32); w, g are recovered at the end;
 //  * lookahead: y_{n+1} = yhat_{n+1} + 2 mu (sum_k u_{n,k} . u_{n+1,k}) e_n, with
 //    yhat computed from the pre-update matrix off the critical path;
-//  * decision: lanes hold up to 4 points; the nearest point comes from one
-//    REDUX.MIN over 32-bit keys (distance bits with the low 7 bits replaced by the
-//    point index: ties within 2^-16 relative are broken by index), D1 is recomputed
-//    exactly from that point, D2 from a second REDUX over exact distance bits.
+//  * decision: one shared-memory load of the cell entry of y.  FAST cells (one
+//    point nearest everywhere in the cell and every other point >= tau farther)
+//    give ref = p_k and gamma = 1 directly; SLOW cells list the <= 4 points that
+//    can be nearest or within tau of it (ascending, so strict < keeps the lowest
+//    index on ties), from which k1, D1 and D2 (second-smallest distance) follow
+//    exactly as in the oracle; cells with longer lists fall back to brute force.
 // ---------------------------------------------------------------------------
+constexpr size_t LMS_LUT_BYTES = (size_t)LMS_LUT_G * LMS_LUT_G * sizeof(float2);
+constexpr int LMS_CHUNK = 5632;  // update steps per shared-memory window of x2
+constexpr size_t LMS_SMEM_MAX = 220 * 1024;  // + static smem <= 227 KB
+static_assert(LMS_LUT_BYTES + (2 * LMS_CHUNK + 16) * sizeof(float2) <= LMS_SMEM_MAX, "LMS smem budget");
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int Q>
+struct Phase {
+  static constexpr int value = Q;
+};
+
+// one warp per chain; shared memory = [LUT (not in PILOT mode)] [x2 window of <= LMS_CHUNK steps]
+template <int MODE>  // 0: DD soft gate, 1: PILOT (known pattern), 2: DD hard (gamma = 1)
 __global__ void __launch_bounds__(32) kk_lms_kernel(LmsArgs a) {
-  __shared__ float2 s_pts[128];
-  for (int i = threadIdx.x; i < a.m; i += blockDim.x) s_pts[i] = a.pts[i];
-  __syncwarp();
-  const int lane = threadIdx.x & 31;
+  extern __shared__ __align__(128) unsigned char lms_smem[];
+  __shared__ float2 s_pts[129];
+  __shared__ __align__(8) uint64_t s_bar;
+  constexpr size_t LUTB = (MODE == 1) ? 0 : LMS_LUT_BYTES;
+  const float2* s_lut = reinterpret_cast<const float2*>(lms_smem);
+  float2* s_win = reinterpret_cast<float2*>(lms_smem + LUTB);
+  const float INF = __int_as_float(0x7f800000);
+  const int lane = threadIdx.x;
   const int c = blockIdx.x;
   if (c >= a.nchains) return;
+  for (int i = lane; i < 129; i += 32) s_pts[i] = (i < a.m) ? a.pts[i] : make_float2(INF, INF);
   const int b = c / a.nsub, sblk = c - b * a.nsub;
   const int64_t n0l = (int64_t)sblk * a.L - a.K;       // first update symbol, buffer-relative
   const int64_t n0 = (int64_t)b * a.n_sym + n0l;       // ... relative to buffer 0 (pattern index)
-  const float INF = __int_as_float(0x7f800000);
-  float2 p[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int idx = lane + 32 * j;
-    p[j] = (idx < a.m) ? s_pts[idx] : make_float2(INF, INF);
+  const float2* xp = a.x2_b0 + (int64_t)b * a.x2_stride + 2 * n0l - 2;  // step s uses xp[2s .. 2s+5]
+  if (lane == 0) {
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
   }
+  __syncwarp();
+  unsigned phase = 0;
+  // copy x2[2 sa - 1 (16-B alignment) .. 2 sb + 6) of steps [sa, sb) (+ the LUT with the first chunk)
+  auto load_window = [&](int sa, int sb, bool with_lut) -> const float2* {
+    const float2* src = xp + 2 * sa - 2;  // W[0] = x of step sa - 1 (its u for the deferred update)
+    const int mis = (int)(((uintptr_t)src >> 3) & 1);  // float2 elements before a 16-B boundary
+    const float2* srca = src - mis;
+    const unsigned n = (unsigned)(2 * (sb - sa) + 8 + mis + 1) & ~1u;
+    if (lane == 0) {
+      if (with_lut) {
+        mbar_expect_tx(&s_bar, (unsigned)LUTB);
+        bulk_copy(lms_smem, a.lut, (unsigned)LUTB, &s_bar);
+      }
+      mbar_expect_tx(&s_bar, n * (unsigned)sizeof(float2));
+      bulk_copy(s_win, srca, n * (unsigned)sizeof(float2), &s_bar);
+      mbar_arrive(&s_bar);
+    }
+    mbar_wait(&s_bar, phase);
+    phase ^= 1u;
+    return s_win + mis;
+  };
   float A[4], B[4], C[4], D[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -567,18 +619,21 @@ __global__ void __launch_bounds__(32) kk_lms_kernel(LmsArgs a) {
     D[k] = w.x - g.x;
   }
   const float mu2 = 2.0f * a.mu;
+  // cell coordinate with the float->int conversion folded into the FFMA: lc is a
+  // half-integer (host), so lc - 1/2 + 2^23 is exact and the single rounding of fmaf
+  // leaves floor(y*linv + lc) (up to round-half-even at exact integers, absorbed by
+  // the 1e-3 cell enlargement of the table) in the low mantissa bits; clamping in the
+  // float domain maps y outside the grid to the brute-force outer ring.
+  const float MAG = 8388608.0f;
+  const float lcx = a.lcx - 0.5f + MAG, lcy = a.lcy - 0.5f + MAG;
+  const float glo = MAG, ghi = MAG + (float)(LMS_LUT_G - 1);
   unsigned gated = 0;
   float esum = 0.f;
   int64_t pidx = 0;
-  if (a.mode == 1) {
+  if (MODE == 1) {
     pidx = (a.n_off0 + n0) % a.P;
     if (pidx < 0) pidx += a.P;
   }
-  // x2 values of a block of 8 steps: step s uses xp[2s .. 2s+3]; prefetch one block ahead
-  const float2* xp = a.x2_b0 + (int64_t)b * a.x2_stride + 2 * n0l - 2;
-  float2 cur[18], nxt[18];
-#pragma unroll
-  for (int j = 0; j < 18; ++j) cur[j] = xp[j];
   auto filt = [&](float2 u0, float2 u1, float2 u2, float2 u3) {
     const float2 uu[4] = {u0, u1, u2, u3};
     float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
@@ -591,71 +646,148 @@ __global__ void __launch_bounds__(32) kk_lms_kernel(LmsArgs a) {
     }
     return make_float2(x0 + x1, y0 + y1);
   };
-  float2 y = filt(cur[3], cur[2], cur[1], cur[0]);
-  for (int s0 = 0; s0 < a.K; s0 += 8) {
+  // One LMS step n (chunk-local j = n - sa).  The x2 window W (W[i] = xp[2 sa - 2 + i])
+  // lives in an 8-register circular buffer R[i & 7]; step j reads W[2j .. 2j+7]:
+  //   u_n = (W[2j+5], W[2j+4], W[2j+3], W[2j+2]),  u_{n+1} = (W[2j+7], W[2j+6], u0, u1),
+  //   u_{n-1} = (W[2j+3], W[2j+2], W[2j+1], W[2j])
+  // and refills the two dead slots with W[2j+8], W[2j+9]; the phase j & 3 is a
+  // compile-time constant of the 4-step unrolled body, so no register is copied.
+  // State on entry: y = y_n, ep = mu2 e_{n-1} (not yet applied to the matrix),
+  // qa = W[2j+3].W[2j+5], qb = W[2j+2].W[2j+4].  In program order: start the cell
+  // lookup of y_n (critical path); independent of it, and filling its latency, apply
+  // the update of e_{n-1} to the matrix and form yhat_{n+1} = M u_{n+1} and r_n; then
+  // resolve the decision, e_n, and y_{n+1} = yhat_{n+1} + r_n e_n.
+  float2 y = make_float2(0.f, 0.f), ep = make_float2(0.f, 0.f);
+  float2 R[8];
 #pragma unroll
-    for (int j = 0; j < 18; ++j) nxt[j] = xp[2 * (s0 + 8) + j];
+  for (int i = 0; i < 8; ++i) R[i] = y;
+  float qa = 0.f, qb = 0.f;
+  auto dot2 = [](float2 u, float2 v) { return fmaf(u.x, v.x, u.y * v.y); };
+  auto step = [&](auto qc, const float2* W, int j) {
+    constexpr int q = decltype(qc)::value;
+    const float2 u0 = R[(2 * q + 5) & 7], u1 = R[(2 * q + 4) & 7], u2 = R[(2 * q + 3) & 7], u3 = R[(2 * q + 2) & 7];
+    const float2 v0 = R[(2 * q + 7) & 7], v1 = R[(2 * q + 6) & 7], w2 = R[(2 * q + 1) & 7], w3 = R[(2 * q) & 7];
+    const float4 nx = *reinterpret_cast<const float4*>(W + 2 * j + 8);
+    float2 ent = make_float2(0.f, 0.f);
+    bool out = false;
+    int pk = 0;
+    if (MODE == 1) {
+      pk = a.pattern[pidx];
+      pidx = (pidx + 1 == a.P) ? 0 : pidx + 1;
+    } else {
+      // masked index (always inside the table, loaded unconditionally); y outside the
+      // grid -> brute force
+      const float fx = fmaf(y.x, a.linv, lcx), fy = fmaf(y.y, a.linv, lcy);
+      const uint32_t cell = ((__float_as_uint(fy) << 10) | (__float_as_uint(fx) << 3)) & ((LMS_LUT_G * LMS_LUT_G - 1) << 3);
+      ent = *reinterpret_cast<const float2*>(reinterpret_cast<const unsigned char*>(s_lut) + cell);
+      out = (fx < glo) | (fx > ghi) | (fy < glo) | (fy > ghi) | (fx != fx) | (fy != fy);
+    }
+    {
+      const float2 pp[4] = {u2, u3, w2, w3};
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      if (s0 + jj < a.K) {
-        const float2 u0 = cur[2 * jj + 3], u1 = cur[2 * jj + 2], u2 = cur[2 * jj + 1], u3 = cur[2 * jj];
-        const float2 v0 = (jj < 7) ? cur[2 * jj + 5] : nxt[3];
-        const float2 v1 = (jj < 7) ? cur[2 * jj + 4] : nxt[2];
-        // off the critical path: yhat_{n+1} (pre-update matrix) and r = 2 mu sum_k u_n,k . u_n+1,k
-        const float2 yh = filt(v0, v1, u0, u1);
-        const float r = mu2 * (fmaf(u0.x, v0.x, u0.y * v0.y) + fmaf(u1.x, v1.x, u1.y * v1.y) +
-                               fmaf(u2.x, u0.x, u2.y * u0.y) + fmaf(u3.x, u1.x, u3.y * u1.y));
-        // decision: local best / second best over this lane's points
-        float d[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float dx = y.x - p[j].x, dy = y.y - p[j].y;
-          d[j] = fmaf(dx, dx, dy * dy);
-        }
-        float l1 = d[0], l2 = INF;
-        int lk = lane;
-#pragma unroll
-        for (int j = 1; j < 4; ++j) {
-          const bool better = d[j] < l1;
-          l2 = better ? l1 : fminf(l2, d[j]);
-          lk = better ? lane + 32 * j : lk;
-          l1 = better ? d[j] : l1;
-        }
-        const unsigned key = (__float_as_uint(l1) & ~127u) | (unsigned)lk;
-        const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
-        const unsigned k1 = kmin & 127u;
-        const float mine2 = ((unsigned)lk == k1) ? l2 : l1;
-        const float d2 = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(mine2)));
-        const float2 pk = s_pts[k1];
-        const float dx1 = y.x - pk.x, dy1 = y.y - pk.y;
-        const float d1 = fmaf(dx1, dx1, dy1 * dy1);
-        float2 ref;
-        float gamma = 1.0f;
-        if (a.mode == 1) {
-          ref = s_pts[a.pattern[pidx]];
-          pidx = (pidx + 1 == a.P) ? 0 : pidx + 1;
-        } else {
-          ref = pk;
-          if (a.mode == 0 && a.inv_tau > 0.f) gamma = fminf(1.0f, fmaxf(d2 - d1, 0.f) * a.inv_tau);
-        }
-        gated += (gamma < 1.0f) ? 1u : 0u;
-        const float2 e = make_float2(gamma * (ref.x - y.x), gamma * (ref.y - y.y));
-        esum = fmaf(e.x, e.x, fmaf(e.y, e.y, esum));
-        const float ex = mu2 * e.x, ey = mu2 * e.y;
-        const float2 uu[4] = {u0, u1, u2, u3};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          A[k] = fmaf(ex, uu[k].x, A[k]);
-          B[k] = fmaf(ex, uu[k].y, B[k]);
-          C[k] = fmaf(ey, uu[k].x, C[k]);
-          D[k] = fmaf(ey, uu[k].y, D[k]);
-        }
-        // y_{n+1} = yhat_{n+1} + r e_n
-        y = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
+      for (int k = 0; k < 4; ++k) {
+        A[k] = fmaf(ep.x, pp[k].x, A[k]);
+        B[k] = fmaf(ep.x, pp[k].y, B[k]);
+        C[k] = fmaf(ep.y, pp[k].x, C[k]);
+        D[k] = fmaf(ep.y, pp[k].y, D[k]);
       }
     }
+    const float2 yh = filt(v0, v1, u0, u1);
+    const float q5 = dot2(u0, v0), q4 = dot2(u1, v1);
+    const float r = mu2 * (((q5 + q4) + qa) + qb);
+    // straight-line FAST assumption (gamma = 1, ref = the cell's point); SLOW cells
+    // (rare) recompute e below.  Keeping yhat, r and y_{n+1} ahead of the branch lets
+    // them fill the latency of the table load.
+    float2 e, yn;
+    if (MODE == 1) {
+      const float2 ref = s_pts[pk];
+      e = make_float2(ref.x - y.x, ref.y - y.y);
+      yn = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
+    } else {
+      e = make_float2(ent.x - y.x, ent.y - y.y);
+      yn = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
+      // the NaN of a SLOW entry propagates into yn (so the branch needs yhat and r first)
+      if (out | isnan(yn.x)) {
+        const uint32_t w = out ? LMS_BRUTE : __float_as_uint(ent.y);
+        float d1 = INF, d2 = INF;
+        int k1 = 0;
+        if (w == LMS_BRUTE) {
+#pragma unroll 1
+          for (int k = 0; k < a.m; ++k) {
+            const float dx = y.x - s_pts[k].x, dy = y.y - s_pts[k].y;
+            const float d = fmaf(dx, dx, dy * dy);
+            const bool bt = d < d1;
+            d2 = bt ? d1 : fminf(d2, d);
+            k1 = bt ? k : k1;
+            d1 = bt ? d : d1;
+          }
+        } else {
 #pragma unroll
-    for (int j = 0; j < 18; ++j) cur[j] = nxt[j];
+          for (int jj = 0; jj < 4; ++jj) {
+            const int k = (int)((w >> (8 * jj)) & 0xffu);  // 128 = padding (point at infinity)
+            const float dx = y.x - s_pts[k].x, dy = y.y - s_pts[k].y;
+            const float d = fmaf(dx, dx, dy * dy);
+            const bool bt = d < d1;
+            d2 = bt ? d1 : fminf(d2, d);
+            k1 = bt ? k : k1;
+            d1 = bt ? d : d1;
+          }
+        }
+        const float2 ref = s_pts[k1];
+        float gamma = 1.0f;
+        if (MODE == 0) gamma = fminf(1.0f, fmaxf(d2 - d1, 0.f) * a.inv_tau);
+        gated += (gamma < 1.0f) ? 1u : 0u;
+        e = make_float2(gamma * (ref.x - y.x), gamma * (ref.y - y.y));
+        yn = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
+      }
+    }
+    esum = fmaf(e.x, e.x, fmaf(e.y, e.y, esum));
+    y = yn;  // y_{n+1}
+    ep = make_float2(mu2 * e.x, mu2 * e.y);
+    qa = q5;
+    qb = q4;
+    R[(2 * q) & 7] = make_float2(nx.x, nx.y);      // W[2j+8]
+    R[(2 * q + 1) & 7] = make_float2(nx.z, nx.w);  // W[2j+9]
+  };
+  using P0 = Phase<0>;
+  using P1 = Phase<1>;
+  using P2 = Phase<2>;
+  using P3 = Phase<3>;
+  const float2* W = nullptr;
+  int n = 0;
+#pragma unroll 1
+  for (int sa = 0; sa < a.K; sa += LMS_CHUNK) {
+    const int sb = min(a.K, sa + LMS_CHUNK);
+    if (sa > 0) __syncwarp();  // every lane is done with the previous window
+    W = load_window(sa, sb, sa == 0 && MODE != 1);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) R[i] = W[i];
+    qa = dot2(R[3], R[5]);
+    qb = dot2(R[2], R[4]);
+    if (sa == 0) y = filt(R[5], R[4], R[3], R[2]);
+    n = sb - sa;
+    const int n4 = n & ~3;
+#pragma unroll 1
+    for (int j = 0; j < n4; j += 4) {
+      step(P0{}, W, j);
+      step(P1{}, W, j + 1);
+      step(P2{}, W, j + 2);
+      step(P3{}, W, j + 3);
+    }
+    if (n4 < n) step(P0{}, W, n4);
+    if (n4 + 1 < n) step(P1{}, W, n4 + 1);
+    if (n4 + 2 < n) step(P2{}, W, n4 + 2);
+  }
+  // the update of the last step: e_{K-1} with u_{K-1} = (W[2n+3], W[2n+2], W[2n+1], W[2n]) of the last window
+  {
+    const float2 lastu[4] = {W[2 * n + 3], W[2 * n + 2], W[2 * n + 1], W[2 * n]};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      A[k] = fmaf(ep.x, lastu[k].x, A[k]);
+      B[k] = fmaf(ep.x, lastu[k].y, B[k]);
+      C[k] = fmaf(ep.y, lastu[k].x, C[k]);
+      D[k] = fmaf(ep.y, lastu[k].y, D[k]);
+    }
   }
   if (lane == 0) {
 #pragma unroll
@@ -664,7 +796,7 @@ __global__ void __launch_bounds__(32) kk_lms_kernel(LmsArgs a) {
       a.taps[(int64_t)c * 8 + k] = make_float2(0.5f * (A[k] + D[k]), 0.5f * (C[k] - B[k]));
       a.taps[(int64_t)c * 8 + 4 + k] = make_float2(0.5f * (A[k] - D[k]), 0.5f * (C[k] + B[k]));
     }
-    atomicAdd(&a.counts[b * 8 + C_GATED], (unsigned long long)gated);
+    if (gated) atomicAdd(&a.counts[b * 8 + C_GATED], (unsigned long long)gated);
     bool bad = !(esum / (float)a.K <= 1.0f);
 #pragma unroll
     for (int k = 0; k < 4; ++k) bad |= !isfinite(A[k] + B[k] + C[k] + D[k]);
@@ -672,9 +804,30 @@ __global__ void __launch_bounds__(32) kk_lms_kernel(LmsArgs a) {
   }
 }
 
+static size_t lms_smem_bytes(int mode, int K) {
+  const size_t lut = (mode == 1) ? 0 : LMS_LUT_BYTES;
+  return lut + (size_t)(2 * min(K, LMS_CHUNK) + 16) * sizeof(float2);
+}
+
+cudaError_t lms_setup() {
+  cudaError_t e = cudaFuncSetAttribute(kk_lms_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LMS_SMEM_MAX);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kk_lms_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LMS_SMEM_MAX);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kk_lms_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LMS_SMEM_MAX);
+  return e;
+}
+
 cudaError_t launch_lms(const LmsArgs& a, cudaStream_t s) {
   if (a.nchains < 1) return cudaSuccess;
-  kk_lms_kernel<<<a.nchains, 32, 0, s>>>(a);
+  const int mode = (a.mode == 1) ? 1 : (a.mode == 2 || !(a.inv_tau > 0.f)) ? 2 : 0;
+  const size_t sm = lms_smem_bytes(mode, a.K);
+  if (mode == 1)
+    kk_lms_kernel<1><<<a.nchains, 32, sm, s>>>(a);
+  else if (mode == 2)
+    kk_lms_kernel<2><<<a.nchains, 32, sm, s>>>(a);
+  else
+    kk_lms_kernel<0><<<a.nchains, 32, sm, s>>>(a);
   return cudaGetLastError();
 }
 

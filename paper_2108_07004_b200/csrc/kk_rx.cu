@@ -49,6 +49,8 @@ struct kk_rx {
   int grid_chain = 0;
   // constant tables
   float2 *d_tw = nullptr, *d_tw512 = nullptr, *d_H = nullptr, *d_pts = nullptr, *d_winit = nullptr;
+  float2* d_lmslut = nullptr;
+  float lms_lcx = 0, lms_lcy = 0, lms_linv = 0;
   uint32_t* d_lut = nullptr;
   DecLut lut{};
   uint8_t *d_lab = nullptr, *d_pattern = nullptr;
@@ -186,6 +188,80 @@ static void build_lut(const std::vector<double>& pts, int m, DecLut& L, std::vec
   }
 }
 
+// LMS update-pass look-up table (kk_internal.h "LmsArgs"): for each cell R (enlarged
+// by 1e-3 of a cell against fp32 index rounding) the list holds every point k with
+//   min_{y in R} |y - p_k|^2  <=  U + tau  (+ slack),   U = min_j max_{y in R} |y - p_j|^2,
+// a superset of the points that can be nearest, or within tau of the nearest, somewhere
+// in R (since D_k(y) - D_1(y) >= min_R D_k - U).  One point => FAST entry (p_k itself);
+// 2..4 points => SLOW entry (NaN, ascending indices, 128-padded); more, or the outer
+// ring of cells (which also receives every clamped y outside the grid) => brute force.
+static void build_lms_lut(const std::vector<double>& pts, int m, double tau, LmsArgs& la, std::vector<float2>& cells,
+                          int* n_fast) {
+  const int G = LMS_LUT_G;
+  double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300, dmin = 1e300;
+  for (int k = 0; k < m; ++k) {
+    xmin = std::min(xmin, pts[2 * k]);
+    xmax = std::max(xmax, pts[2 * k]);
+    ymin = std::min(ymin, pts[2 * k + 1]);
+    ymax = std::max(ymax, pts[2 * k + 1]);
+    for (int j = 0; j < k; ++j)
+      dmin = std::min(dmin, std::hypot(pts[2 * k] - pts[2 * j], pts[2 * k + 1] - pts[2 * j + 1]));
+  }
+  const double pad = 2.0 * dmin;
+  const double span = std::max(xmax - xmin, ymax - ymin) + 2 * pad;
+  const float linv = (float)(G / span);
+  // half-integer origins: the kernel adds 2^23 - 1/2 to lc, which must stay exact in fp32
+  const float lcx = (float)(std::floor(-(xmin - pad) * (double)linv) + 0.5);
+  const float lcy = (float)(std::floor(-(ymin - pad) * (double)linv) + 0.5);
+  la.linv = linv;
+  la.lcx = lcx;
+  la.lcy = lcy;
+  const double cs = 1.0 / (double)linv;
+  cells.assign((size_t)G * G, make_float2(0.f, 0.f));
+  std::vector<double> mind(m);
+  int nf = 0;
+  const uint32_t nan_bits = 0x7fc00000u;
+  for (int cy = 0; cy < G; ++cy)
+    for (int cx = 0; cx < G; ++cx) {
+      float2 ent;
+      std::memcpy(&ent.x, &nan_bits, 4);
+      uint32_t w = LMS_BRUTE;
+      if (cx > 0 && cy > 0 && cx < G - 1 && cy < G - 1) {
+        const double e = 1e-3 * cs;
+        const double xl = (cx - (double)lcx) * cs - e, xh = (cx + 1 - (double)lcx) * cs + e;
+        const double yl = (cy - (double)lcy) * cs - e, yh = (cy + 1 - (double)lcy) * cs + e;
+        double U = 1e300;
+        for (int k = 0; k < m; ++k) {
+          const double px = pts[2 * k], py = pts[2 * k + 1];
+          const double dx = std::max(0.0, std::max(xl - px, px - xh)), dy = std::max(0.0, std::max(yl - py, py - yh));
+          mind[k] = dx * dx + dy * dy;
+          const double fx = std::max(std::fabs(px - xl), std::fabs(px - xh)),
+                       fy = std::max(std::fabs(py - yl), std::fabs(py - yh));
+          U = std::min(U, fx * fx + fy * fy);
+        }
+        const double lim = U + tau + 1e-5 * (1.0 + U);
+        int cnt = 0, first = -1;
+        uint32_t lw = 0x80808080u;
+        for (int k = 0; k < m; ++k)
+          if (mind[k] <= lim) {
+            if (cnt < 4) lw = (lw & ~(0xffu << (8 * cnt))) | ((uint32_t)k << (8 * cnt));
+            if (first < 0) first = k;
+            ++cnt;
+          }
+        if (cnt == 1) {
+          ent = make_float2((float)pts[2 * first], (float)pts[2 * first + 1]);
+          ++nf;
+          cells[(size_t)cy * G + cx] = ent;
+          continue;
+        }
+        if (cnt >= 2 && cnt <= 4) w = lw;
+      }
+      std::memcpy(&ent.y, &w, 4);
+      cells[(size_t)cy * G + cx] = ent;
+    }
+  if (n_fast) *n_fast = nf;
+}
+
 extern "C" {
 
 int kk_rx_abi_version(void) { return KK_RX_ABI_VERSION; }
@@ -222,6 +298,36 @@ int kk_rx_constellation(int fmt, float* points_out, uint8_t* labels_out) {
   return m;
 }
 
+int kk_rx_decision_tables(const float* points, int m, float tau, float* lms_cells, float* lms_geom, uint32_t* dec_cells,
+                          float* dec_geom) {
+  if (!points || m < 2 || m > 128) {
+    g_err = "need 2..128 points";
+    return -1;
+  }
+  std::vector<double> pts(2 * m);
+  for (int k = 0; k < 2 * m; ++k) pts[k] = points[k];
+  LmsArgs la{};
+  std::vector<float2> lc;
+  build_lms_lut(pts, m, tau > 0.f ? (double)tau : 0.0, la, lc, nullptr);
+  if (lms_cells) std::memcpy(lms_cells, lc.data(), lc.size() * sizeof(float2));
+  if (lms_geom) {
+    lms_geom[0] = la.lcx;
+    lms_geom[1] = la.lcy;
+    lms_geom[2] = la.linv;
+  }
+  DecLut L{};
+  std::vector<uint32_t> dc;
+  build_lut(pts, m, L, dc);
+  if (dec_cells && !dc.empty()) std::memcpy(dec_cells, dc.data(), dc.size() * sizeof(uint32_t));
+  if (dec_geom) {
+    dec_geom[0] = L.x0;
+    dec_geom[1] = L.y0;
+    dec_geom[2] = L.inv;
+    dec_geom[3] = (float)L.g;
+  }
+  return LMS_LUT_G;
+}
+
 kk_status kk_rx_halo_for(int64_t buffer_len, int32_t k_update, int64_t* left, int64_t* right) {
   if (!left || !right || buffer_len <= 0 || k_update <= 0) return fail(KK_EINVAL, "bad arguments");
   halo_geometry(buffer_len, k_update, left, right, nullptr, nullptr, nullptr);
@@ -236,7 +342,7 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
   void* ptrs[] = {h->d_tw,     h->d_tw512,  h->d_H,      h->d_pts,    h->d_winit,    h->d_lut,
-                  h->d_lab,    h->d_pattern, h->d_tails, h->d_taps,   h->d_counts,   h->d_out,
+                  h->d_lab,    h->d_pattern, h->d_lmslut, h->d_tails, h->d_taps,   h->d_counts,   h->d_out,
                   h->d_x2full, h->d_es,     h->d_stage[0], h->d_stage[1]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -460,7 +566,21 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
       h->lut.cell = h->d_lut;
     }
   }
+  {
+    // LMS look-up table: tau of the soft gate, 0 for the hard / PILOT modes
+    std::vector<float2> cells;
+    LmsArgs tmp{};
+    const double tau_lut = (h->mode == KK_UPD_DD_SOFT && h->tau > 0.f) ? (double)h->tau : 0.0;
+    int nf = 0;
+    build_lms_lut(pts, m, tau_lut, tmp, cells, &nf);
+    h->lms_lcx = tmp.lcx;
+    h->lms_lcy = tmp.lcy;
+    h->lms_linv = tmp.linv;
+    CKC(cudaMalloc(&h->d_lmslut, cells.size() * sizeof(float2)));
+    CKC(cudaMemcpy(h->d_lmslut, cells.data(), cells.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
   CKC(chain_setup(dev, &h->grid_chain));
+  CKC(lms_setup());
   CKC(cudaGetLastError());
 #undef CKC
   *out = h;
@@ -587,6 +707,10 @@ static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int
       la.x2_b0 = x2f0;
       la.x2_stride = h->N / 2;
     }
+    la.lut = h->d_lmslut;
+    la.lcx = h->lms_lcx;
+    la.lcy = h->lms_lcy;
+    la.linv = h->lms_linv;
     la.n_sym = h->n_sym;
     la.L = h->L;
     la.nsub = h->nsub;
