@@ -42,10 +42,29 @@ __device__ __forceinline__ uint32_t tone_index(const ChainArgs& a, int64_t pos) 
   return (uint32_t)r;
 }
 
+// MUFU forms without the denormal fix-ups of the CUDA math wrappers (arguments here are
+// >= v_min > 0, far from the denormal range)
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// sin/cos of an angle that needs no range reduction (|x| of a few pi: the hardware
+// works in turns, so only the fp32 precision of x / 2 pi matters)
+__device__ __forceinline__ void sincos_small(float x, float* s, float* c) {
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(*s) : "f"(x));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(*c) : "f"(x));
+}
+
 __device__ __forceinline__ void cis_turns(float t, float* s, float* c) {
   // e^{2 pi i t} for any t, with exact reduction to [-1/2, 1/2] before __sincosf
   t -= rintf(t);
-  __sincosf(t * 6.2831853071795865f, s, c);
+  sincos_small(t * 6.2831853071795865f, s, c);
 }
 
 // Exact minimum-distance decision (ties -> lowest index, reading R11): the LUT
@@ -303,7 +322,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
 #pragma unroll
           for (int j = 0; j < 48; ++j) {
             const float vv = fmaxf((float)src[re0 + lane + 32 * j] + a.dc, a.vmin);
-            const float l = __log2f(vv * invd) * 0.34657359027997264f;  // 0.5 * ln 2
+            // 0.5 ln 2 / 1024: the 1/1024 of the inverse FFT is folded in here
+            const float l = lg2_ftz(vv * invd) * (0.34657359027997264f / 1024.0f);
             if (j < 32) v[brev(j, 5)].x = l;        // FFT input registers are bit-reversed
             if (j >= 16) v[brev(j - 16, 5)].y = l;
           }
@@ -320,14 +340,13 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
         for (int f = 0; f < nfft; ++f) {
           fft1024(v, lane, scr, s_tw);
           if (isH && f == 0) {
-            // S2: phi = -H{l} <-> +i sgn(k) L_k (reading R1), /1024, conjugated so the
+            // S2: phi = -H{l} <-> +i sgn(k) L_k (reading R1; the /1024 is in S1), conjugated so the
             // next forward FFT computes the inverse: IFFT(Y) = conj(FFT(conj(Y)))
-            const float sc = 1.0f / 1024.0f;
             float2 nv[32];
 #pragma unroll
             for (int k2 = 0; k2 < 32; ++k2) {
               const float2 y = v[k2];
-              float2 r = (k2 < 16) ? make_float2(-y.y * sc, -y.x * sc) : make_float2(y.y * sc, y.x * sc);
+              float2 r = (k2 < 16) ? make_float2(-y.y, -y.x) : make_float2(y.y, y.x);
               if ((k2 == 0 || k2 == 16) && lane == 0) r = make_float2(0.f, 0.f);
               nv[brev(k2, 5)] = r;  // bit-reversed input of the next transform
             }
@@ -358,9 +377,9 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
             const float phi = dst[mm].y;
             const int16_t code = src[s_off + mm];
             const float vv = fmaxf((float)code + a.dc, a.vmin);
-            const float amp = vv * rsqrtf(vv);
+            const float amp = vv * rsqrt_ftz(vv);
             float sp, cp;
-            cis_turns(phi * 0.15915494309189535f, &sp, &cp);
+            sincos_small(phi, &sp, &cp);  // |phi| of a few rad at most (KK phase)
             dst[mm] = make_float2(fmaf(amp, cp, -a.a_hat), amp * sp);
             clip += ((float)code + a.dc < a.vmin && mm < lim) ? 1u : 0u;
           }
