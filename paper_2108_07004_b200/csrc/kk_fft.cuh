@@ -169,7 +169,7 @@ __device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __rest
 // Forward 512-point DFT of the folded spectrum, one warp:
 //   in : Z[lane + 32*k2] at z[brev4(k2)], k2 in [0,16)   (registers bit-reversed)
 //   out: lane (2*r1 + h) gets z[r2] = X[r1 + 16*(r2 + 16*h)],  X[r] = sum_k Z[k] e^{-2 pi i k r / 512}
-// scr: this warp's tile (>= 16 x 34 floats); tw512[r1*32 + l] = e^{-2 pi i r1 l / 512} (global, L1).
+// scr: this warp's tile (>= 16 x 34 floats); tw512[r1*32 + l] = e^{-2 pi i r1 l / 512} (shared).
 // The inverse transform the method needs is conj(DFT(conj(Z))), done by the caller.
 __device__ __forceinline__ void fft512_pairs(float2 (&z)[16], int lane, float* __restrict__ scr,
                                              const float2* __restrict__ tw512) {
@@ -179,7 +179,7 @@ __device__ __forceinline__ void fft512_pairs(float2 (&z)[16], int lane, float* _
     dft_brin<16>(z);
     if (pass == 0) {
 #pragma unroll
-      for (int r = 1; r < 16; ++r) z[r] = c_mul(z[r], __ldg(tw512 + r * 32 + lane));
+      for (int r = 1; r < 16; ++r) z[r] = c_mul(z[r], tw512[r * 32 + lane]);
 #pragma unroll
       for (int r = 0; r < 16; ++r) scr[r * 34 + lane] = z[r].x;
       __syncwarp();

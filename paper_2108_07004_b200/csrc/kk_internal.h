@@ -17,7 +17,8 @@ constexpr int EBUF = STEP + 256;    // D = E_tf - A_hat window of one step: [307
 constexpr int STG = STEP + 512;     // codes of one step: [3072 i - 256, 3072 i + 3328)
 constexpr int WARM = 1536;          // warm-up codes: [3072 i - 1280, 3072 i + 256)
 constexpr int XS = 1538;            // x2 window of one step (APPLY): positions 3072 i - 132 + 2 j
-constexpr int NWARPS = 4;
+constexpr int NWARPS = 4;          // warps per group
+constexpr int NGROUP = 4;          // independent groups per CTA (one CTA per SM)
 constexpr int TILE = 32 * 33;       // per-warp transpose tile (floats)
 constexpr int SYM_PER_STEP = 768;
 constexpr int MAX_SEG = 4;
@@ -68,6 +69,7 @@ struct ChainArgs {
   const uint8_t* labels;   // [m]
   const uint8_t* pattern;  // [P] or nullptr
   int64_t P;
+  int32_t pat_tma;         // pattern staged by bulk copies (P % 16 == 0)
   DecLut lut;
 };
 

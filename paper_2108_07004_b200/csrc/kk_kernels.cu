@@ -20,11 +20,20 @@
 
 namespace kk {
 
-constexpr size_t SMEM_TW = 1024 * sizeof(float2);
+// one CTA per SM = NGROUP independent 4-warp groups (each the former 128-thread CTA,
+// synchronised by its own named barrier) sharing one copy of the read-only tables
+constexpr size_t SMEM_TW = 1024 * sizeof(float2);     // 1024-pt twiddles
+constexpr size_t SMEM_H = 1024 * sizeof(float2);      // static-EQ spectrum Hs
+constexpr size_t SMEM_TW512 = 512 * sizeof(float2);   // 512-pt twiddles
+constexpr size_t SMEM_LUT = 64 * 64 * sizeof(uint32_t);  // decision table (g <= 64)
+constexpr size_t SMEM_SHARED = SMEM_TW + SMEM_H + SMEM_TW512 + SMEM_LUT;
 constexpr size_t SMEM_EBUF = EBUF * sizeof(float2);
 constexpr size_t SMEM_STG = STG * sizeof(int16_t);
 constexpr size_t SMEM_XS = XS * sizeof(float2);  // also holds the warm-up codes (WARM int16)
-constexpr size_t CHAIN_SMEM = SMEM_TW + SMEM_EBUF + SMEM_STG + SMEM_XS + 16;
+constexpr size_t SMEM_PAT = 832;                 // pattern bytes of one step (768 + alignment)
+constexpr size_t SMEM_GROUP = SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT + 64 + 16;  // + factored WL taps + mbarriers
+constexpr size_t CHAIN_SMEM = SMEM_SHARED + NGROUP * SMEM_GROUP;
+static_assert(SMEM_GROUP % 16 == 0 && SMEM_SHARED % 16 == 0, "16-B aligned regions");
 static_assert(WARM * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-up codes + tile must fit the x2 window");
 static_assert(TILE * sizeof(float) <= EQ_KEEP * sizeof(float2), "transpose tile must fit an EQ stride of ebuf");
 
@@ -72,11 +81,14 @@ __device__ __forceinline__ void cis_turns(float t, float* s, float* c) {
 // (slightly enlarged) cell; brute force outside the grid or for crowded cells.
 constexpr uint32_t LUT_BRUTE = 1u << 31;
 
-__device__ __forceinline__ uint32_t lut_word(float2 y, const DecLut& L) {
+// table in shared memory (s_cells, g <= 64) or global (L.cell)
+__device__ __forceinline__ uint32_t lut_word(float2 y, const DecLut& L, const uint32_t* s_cells, bool in_smem) {
   if (L.g > 0) {
     const float fx = (y.x - L.x0) * L.inv, fy = (y.y - L.y0) * L.inv;
-    if (fx >= 0.f && fy >= 0.f && fx < (float)L.g && fy < (float)L.g)
-      return __ldg(L.cell + (int)fy * L.g + (int)fx);
+    if (fx >= 0.f && fy >= 0.f && fx < (float)L.g && fy < (float)L.g) {
+      const int c = (int)fy * L.g + (int)fx;
+      return in_smem ? s_cells[c] : __ldg(L.cell + c);
+    }
   }
   return LUT_BRUTE;
 }
@@ -116,7 +128,7 @@ __device__ __forceinline__ int decide_word(float2 y, uint32_t w, const float2* _
 }
 
 __device__ __forceinline__ int decide(float2 y, const DecLut& L, const float2* __restrict__ sp, int m) {
-  return decide_word(y, lut_word(y, L), sp, m);
+  return decide_word(y, lut_word(y, L, nullptr, false), sp, m);
 }
 
 __device__ __forceinline__ float2 wl_out(const float2 (&w)[4], const float2 (&g)[4], float2 u0, float2 u1, float2 u2,
@@ -133,6 +145,11 @@ __device__ __forceinline__ float2 wl_out(const float2 (&w)[4], const float2 (&g)
 }
 
 __device__ __forceinline__ unsigned warp_sum(unsigned v) { return __reduce_add_sync(0xffffffffu, v); }
+
+// named barrier of one 4-warp group (ids 1..NGROUP; 0 is __syncthreads)
+__device__ __forceinline__ void group_sync(int gi) {
+  asm volatile("bar.sync %0, %1;" ::"r"(gi + 1), "r"(NWARPS * 32) : "memory");
+}
 
 // --- TMA bulk copy + mbarrier helpers (sm_90+)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -157,6 +174,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 struct StepPos {
@@ -191,43 +221,58 @@ __device__ __forceinline__ StepPos decode_step(const ChainArgs& a, int64_t g) {
 //   phase E: 4 static-EQ blocks (one per warp): S4 -> x2 (smem or HBM)
 //   phase A: 768 symbols of S5' + S6 + S7 (APPLY segments)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(ChainArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* s_tw = reinterpret_cast<float2*>(smem_raw);
-  float2* ebuf = reinterpret_cast<float2*>(smem_raw + SMEM_TW);
-  int16_t* stg = reinterpret_cast<int16_t*>(smem_raw + SMEM_TW + SMEM_EBUF);
-  float2* xs = reinterpret_cast<float2*>(smem_raw + SMEM_TW + SMEM_EBUF + SMEM_STG);
+  float2* s_H = reinterpret_cast<float2*>(smem_raw + SMEM_TW);
+  float2* s_tw512 = reinterpret_cast<float2*>(smem_raw + SMEM_TW + SMEM_H);
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem_raw + SMEM_TW + SMEM_H + SMEM_TW512);
+  const int gi = threadIdx.x / (NWARPS * 32);      // group of this thread
+  const int tid = threadIdx.x % (NWARPS * 32);     // thread index inside the group
+  unsigned char* gbase = smem_raw + SMEM_SHARED + (size_t)gi * SMEM_GROUP;
+  float2* ebuf = reinterpret_cast<float2*>(gbase);
+  int16_t* stg = reinterpret_cast<int16_t*>(gbase + SMEM_EBUF);
+  float2* xs = reinterpret_cast<float2*>(gbase + SMEM_EBUF + SMEM_STG);
+  uint8_t* spat = gbase + SMEM_EBUF + SMEM_STG + SMEM_XS;
   int16_t* wstg = reinterpret_cast<int16_t*>(xs);  // warm-up codes (H phase only)
   float* wscr = reinterpret_cast<float*>(xs + WARM / 4);  // warm-up task's transpose tile
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + SMEM_TW + SMEM_EBUF + SMEM_STG + SMEM_XS);
+  float2* s_taps = reinterpret_cast<float2*>(gbase + SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT);  // ta[4], tc[4]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(gbase + SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT + 64);
+  uint64_t* pbar = bar + 1;
   __shared__ float2 s_pts[128];
   __shared__ uint8_t s_lab[128];
 
-  for (int k = threadIdx.x; k < 1024; k += blockDim.x) s_tw[k] = a.tw1024[k];
+  for (int k = threadIdx.x; k < 1024; k += blockDim.x) {
+    s_tw[k] = a.tw1024[k];
+    s_H[k] = a.Hs[k];
+  }
+  for (int k = threadIdx.x; k < 512; k += blockDim.x) s_tw512[k] = a.tw512[k];
+  const bool lut_smem = a.lut.g > 0 && a.lut.g <= 64;
+  if (lut_smem)
+    for (int k = threadIdx.x; k < a.lut.g * a.lut.g; k += blockDim.x) s_lut[k] = a.lut.cell[k];
   for (int k = threadIdx.x; k < a.m; k += blockDim.x) {
     s_pts[k] = a.pts[k];
     s_lab[k] = a.labels[k];
   }
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     mbar_init(bar, 1);
+    mbar_init(pbar, 1);
     mbar_fence_init();
   }
   __syncthreads();
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = tid >> 5, lane = tid & 31;
   const float invd = 1.0f / a.dc;
   const uint32_t n32 = (uint32_t)a.N;
-  const int64_t g0 = (int64_t)blockIdx.x * a.total_steps / gridDim.x;
-  const int64_t g1 = (int64_t)(blockIdx.x + 1) * a.total_steps / gridDim.x;
+  const int64_t ngroups = (int64_t)gridDim.x * NGROUP, grp = (int64_t)blockIdx.x * NGROUP + gi;
+  const int64_t g0 = grp * a.total_steps / ngroups;
+  const int64_t g1 = (grp + 1) * a.total_steps / ngroups;
+  unsigned pphase = 0;
   int prev_s = -1, prev_o = -1000000;
   int64_t prev_i = -1000000;
   unsigned acc_clip = 0, acc_se = 0, acc_be = 0;
   unsigned phase_bit = 0;
   bool prefetched = false;
-  // WL taps of the current owner, factored: y.x = sum ta.x u.x + ta.y u.y, y.y = sum tc.x u.x + tc.y u.y
-  float2 ta[4], tc[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) ta[k] = tc[k] = make_float2(0.f, 0.f);
 
   auto flush = [&](int s, int o) {
     if (s < 0) return;
@@ -259,14 +304,13 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
     const bool next_cont = (g + 1 < g1) && nxt.s == s && nxt.o == owner && nxt.i == i + 1;
     if (s != prev_s || owner != prev_o) {
       flush(prev_s, prev_o);
-      if (mode == SEG_APPLY) {
+      if (mode == SEG_APPLY && tid < 4) {
+        // WL taps of the new owner, factored: y.x = sum ta.x u.x + ta.y u.y, y.y = sum tc.x u.x + tc.y u.y
+        // (kept in shared memory: only phase A reads them)
         const float2* tp = sg.taps + (int64_t)(owner - sg.owner_first) * 8;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 w = tp[k], gg = tp[4 + k];
-          ta[k] = make_float2(w.x + gg.x, gg.y - w.y);
-          tc[k] = make_float2(w.y + gg.y, w.x - gg.x);
-        }
+        const float2 w = tp[tid], gg = tp[4 + tid];
+        s_taps[tid] = make_float2(w.x + gg.x, gg.y - w.y);
+        s_taps[4 + tid] = make_float2(w.y + gg.y, w.x - gg.x);
       }
     }
     const int16_t* obase = a.codes + (int64_t)owner * a.N;
@@ -281,20 +325,36 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
     } else if (a.aligned16) {
       const uint4* s4 = reinterpret_cast<const uint4*>(obase + sbase);
       uint4* d4 = reinterpret_cast<uint4*>(stg);
-      for (int k = threadIdx.x; k < STG / 8; k += blockDim.x) d4[k] = __ldg(s4 + k);
+      for (int k = tid; k < STG / 8; k += NWARPS * 32) d4[k] = __ldg(s4 + k);
     } else {
-      for (int k = threadIdx.x; k < STG; k += blockDim.x) stg[k] = obase[sbase + k];
+      for (int k = tid; k < STG; k += NWARPS * 32) stg[k] = obase[sbase + k];
     }
     if (warm) {
       if (a.aligned16) {
         const uint4* s4 = reinterpret_cast<const uint4*>(obase + wbase);
         uint4* d4 = reinterpret_cast<uint4*>(wstg);
-        for (int k = threadIdx.x; k < WARM / 8; k += blockDim.x) d4[k] = __ldg(s4 + k);
+        for (int k = tid; k < WARM / 8; k += NWARPS * 32) d4[k] = __ldg(s4 + k);
       } else {
-        for (int k = threadIdx.x; k < WARM; k += blockDim.x) wstg[k] = obase[wbase + k];
+        for (int k = tid; k < WARM; k += NWARPS * 32) wstg[k] = obase[wbase + k];
       }
     }
-    __syncthreads();
+    // pattern bytes of this step's symbols (APPLY with counting): bulk copy, waited for in phase A
+    const bool count_ref = (mode == SEG_APPLY) && a.pattern != nullptr;
+    if (count_ref && a.pat_tma) {
+      if (tid == 0) {
+        int64_t pb = (sg.n_off + (int64_t)(owner - sg.owner_first) * a.n_sym + (int64_t)SYM_PER_STEP * i - 32) % a.P;
+        if (pb < 0) pb += a.P;
+        const int64_t pa = pb & ~(int64_t)15;
+        const unsigned len = (unsigned)(((pb - pa) + SYM_PER_STEP + 15) & ~15);
+        const unsigned len1 = (pa + len <= a.P) ? len : (unsigned)(a.P - pa);
+        fence_proxy_async();
+        mbar_expect_tx(pbar, len);
+        bulk_copy(spat, a.pattern + pa, len1, pbar);
+        if (len1 < len) bulk_copy(spat + len1, a.pattern, len - len1, pbar);
+        mbar_arrive(pbar);
+      }
+    }
+    group_sync(gi);
 
     // ---- phase 0: Hilbert pairs (warps 0-2, warp 3 = warm-up pair); phase 1: EQ blocks
 #pragma unroll 1
@@ -303,7 +363,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
       if (!isH) {
         // stg is free now: prefetch the next step's codes (async proxy) behind phases E and A
         prefetched = next_cont && a.aligned16;
-        if (prefetched && threadIdx.x == 0) {
+        if (prefetched && tid == 0) {
           fence_proxy_async();
           bulk_load(stg, obase + sbase + STEP, STG * sizeof(int16_t), bar);
         }
@@ -334,7 +394,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
         // transpose tile: H tasks use their own (not yet written) output slice of ebuf,
         // the warm-up task a slice of xs; E tasks reuse ebuf once every window is loaded.
         float* scr = wt ? wscr : reinterpret_cast<float*>(ebuf + (isH ? 256 + 1024 * warp : EQ_KEEP * warp));
-        if (!isH) __syncthreads();  // all E windows are in registers before ebuf becomes scratch
+        if (!isH) group_sync(gi);  // all E windows are in registers before ebuf becomes scratch
         const int nfft = isH ? 2 : 1;
 #pragma unroll 1
         for (int f = 0; f < nfft; ++f) {
@@ -412,11 +472,11 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
           float2 z[16];
 #pragma unroll
           for (int k2 = 0; k2 < 16; ++k2) {
-            const float2 s0 = c_mul(v[k2], __ldg(a.Hs + lane + 32 * k2));
-            const float2 s1 = c_mul(v[k2 + 16], __ldg(a.Hs + lane + 32 * (k2 + 16)));
+            const float2 s0 = c_mul(v[k2], s_H[lane + 32 * k2]);
+            const float2 s1 = c_mul(v[k2 + 16], s_H[lane + 32 * (k2 + 16)]);
             z[brev(k2, 4)] = make_float2(s0.x + s1.x, -(s0.y + s1.y));  // conj -> forward DFT = inverse
           }
-          fft512_pairs(z, lane, scr, a.tw512);
+          fft512_pairs(z, lane, scr, s_tw512);
           const int h = lane & 1, r1 = lane >> 1;
           // lane holds window outputs rr = r1 + 16 r2 + 256 h, i.e. positions P = P0 + 2 rr: a
           // stride-16 run in x2 index; keep rr in [rlo, 448) and (X2 modes) the owned positions
@@ -459,28 +519,34 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
           }
         }
       }
-      __syncthreads();
+      group_sync(gi);
     }
 
     if (mode == SEG_APPLY) {
       // ---- S5' + S6 + S7 on symbols [768 i - 32, 768 i + 736) of this owner
-      const int64_t nbase = (int64_t)SYM_PER_STEP * i - 32;
+      const int nbase = SYM_PER_STEP * (int)i - 32;
       const int64_t ko = owner - sg.owner_first;
-      int64_t pb = 0;
-      if (a.pattern) {
-        pb = (sg.n_off + ko * a.n_sym + nbase) % a.P;
-        if (pb < 0) pb += a.P;
-      }
       uint8_t* outp = sg.out + ko * a.n_sym;
       constexpr int SPT = SYM_PER_STEP / (NWARPS * 32);  // symbols per thread per step (6)
       int refv[SPT];
-      if (a.pattern) {
-        // pattern bytes first: these L2 loads are in flight while y and the LUT words are formed
+      if (count_ref) {
+        if (a.pat_tma) {
+          mbar_wait(pbar, pphase);
+          pphase ^= 1u;
+          int64_t pb = (sg.n_off + ko * a.n_sym + nbase) % a.P;
+          if (pb < 0) pb += a.P;
+          const int off = (int)(pb & 15);
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-          int64_t pi = pb + threadIdx.x + NWARPS * 32 * k;
-          while (pi >= a.P) pi -= a.P;
-          refv[k] = a.pattern[pi];
+          for (int k = 0; k < SPT; ++k) refv[k] = spat[off + tid + NWARPS * 32 * k];
+        } else {
+          int64_t pb = (sg.n_off + ko * a.n_sym + nbase) % a.P;
+          if (pb < 0) pb += a.P;
+#pragma unroll
+          for (int k = 0; k < SPT; ++k) {
+            int64_t pi = pb + tid + NWARPS * 32 * k;
+            while (pi >= a.P) pi -= a.P;
+            refv[k] = a.pattern[pi];
+          }
         }
       }
       float2 yv[SPT];
@@ -488,26 +554,27 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
         // y = w^T u + g^T u* with u = (xs[2s+3], xs[2s+2], xs[2s+1], xs[2s]), factored taps
-        const int sidx = threadIdx.x + NWARPS * 32 * k;
+        const int sidx = tid + NWARPS * 32 * k;
         const float2 u[4] = {xs[2 * sidx + 3], xs[2 * sidx + 2], xs[2 * sidx + 1], xs[2 * sidx]};
         float2 y = make_float2(0.f, 0.f);
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          y.x = fmaf(ta[t].x, u[t].x, fmaf(ta[t].y, u[t].y, y.x));
-          y.y = fmaf(tc[t].x, u[t].x, fmaf(tc[t].y, u[t].y, y.y));
+          const float2 ta = s_taps[t], tc = s_taps[4 + t];
+          y.x = fmaf(ta.x, u[t].x, fmaf(ta.y, u[t].y, y.x));
+          y.y = fmaf(tc.x, u[t].x, fmaf(tc.y, u[t].y, y.y));
         }
         yv[k] = y;
-        cw[k] = lut_word(y, a.lut);
+        cw[k] = lut_word(y, a.lut, s_lut, lut_smem);
       }
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
-        const int sidx = threadIdx.x + NWARPS * 32 * k;
-        const int64_t n = nbase + sidx;
-        if (n >= 0 && n < a.n_sym) {
+        const int sidx = tid + NWARPS * 32 * k;
+        const int n = nbase + sidx;
+        if (n >= 0 && n < (int)a.n_sym) {
           const int d = decide_word(yv[k], cw[k], s_pts, a.m);
           const uint8_t ld = s_lab[d];
           outp[n] = ld;
-          if (a.pattern) {
+          if (count_ref) {
             acc_se += (refv[k] != d) ? 1u : 0u;
             acc_be += __popc((unsigned)(ld ^ s_lab[refv[k]]));
           }
@@ -515,8 +582,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 4) kk_chain_kernel(ChainArgs a) {
       }
     }
     // keep the last 256 D samples for the next step's first EQ window
-    for (int k = threadIdx.x; k < 256; k += blockDim.x) ebuf[k] = ebuf[STEP + k];
-    __syncthreads();
+    for (int k = tid; k < 256; k += NWARPS * 32) ebuf[k] = ebuf[STEP + k];
+    group_sync(gi);
     prev_s = s;
     prev_o = owner;
     prev_i = i;
@@ -530,7 +597,7 @@ cudaError_t chain_setup(int device, int* grid_out) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaError_t e = cudaFuncSetAttribute(kk_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM);
   if (e != cudaSuccess) return e;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk_chain_kernel, NWARPS * 32, CHAIN_SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk_chain_kernel, NGROUP * NWARPS * 32, CHAIN_SMEM);
   if (occ < 1) occ = 1;
   *grid_out = sms * occ;
   return cudaGetLastError();
@@ -539,7 +606,7 @@ cudaError_t chain_setup(int device, int* grid_out) {
 cudaError_t launch_chain(const ChainArgs& a, int grid, cudaStream_t s) {
   if (a.total_steps <= 0) return cudaSuccess;
   if (grid > a.total_steps) grid = (int)a.total_steps;
-  kk_chain_kernel<<<grid, NWARPS * 32, CHAIN_SMEM, s>>>(a);
+  kk_chain_kernel<<<grid, NGROUP * NWARPS * 32, CHAIN_SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -566,19 +633,6 @@ constexpr size_t LMS_LUT_BYTES = (size_t)LMS_LUT_G * LMS_LUT_G * sizeof(float2);
 constexpr int LMS_CHUNK = 5632;  // update steps per shared-memory window of x2
 constexpr size_t LMS_SMEM_MAX = 220 * 1024;  // + static smem <= 227 KB
 static_assert(LMS_LUT_BYTES + (2 * LMS_CHUNK + 16) * sizeof(float2) <= LMS_SMEM_MAX, "LMS smem budget");
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 template <int Q>
 struct Phase {

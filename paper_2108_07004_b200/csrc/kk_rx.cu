@@ -630,6 +630,7 @@ static void fill_chain_common(kk_rx_t* h, ChainArgs& ca, const int16_t* codes_de
   ca.labels = h->d_lab;
   ca.pattern = h->has_pattern ? h->d_pattern : nullptr;
   ca.P = h->P;
+  ca.pat_tma = h->has_pattern && (h->P % 16 == 0);
   ca.lut = h->lut;
 }
 
