@@ -261,7 +261,10 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
   }
   __syncthreads();
 
-  const int warp = tid >> 5, lane = tid & 31;
+  // task role of this warp inside its group, rotated by the group index: warp w of the
+  // CTA issues on sub-partition w % 4 and phase H leaves one role idle, so without the
+  // rotation all four idle warps would share one sub-partition
+  const int warp = ((tid >> 5) + gi) & (NWARPS - 1), lane = tid & 31;
   const float invd = 1.0f / a.dc;
   const uint32_t n32 = (uint32_t)a.N;
   const int64_t ngroups = (int64_t)gridDim.x * NGROUP, grp = (int64_t)blockIdx.x * NGROUP + gi;
