@@ -9,6 +9,9 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkkrx.so")
+# A/B measurements of kernel variants (tools/gpu/ab.sh): another in-tree build of the same library
+if os.environ.get("KKRX_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["KKRX_LIB"])
 
 KK_OK, KK_EINVAL, KK_ENOMEM, KK_ECUDA, KK_ESTATE, KK_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 FORMATS = {"QAM4": 0, "QAM8": 1, "QAM16": 2, "QAM32": 3, "QAM64": 4, "QAM128": 5, "GS8": 6, "GS128": 7,

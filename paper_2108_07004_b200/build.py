@@ -16,22 +16,27 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompil
 SOURCES = ["kk_rx.cu", "kk_kernels.cu", "kk_constellation.cpp"]
 
 
-def build(verbose=False, force=False):
-    srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    deps.append(os.path.join(os.path.dirname(HERE), "include", "kk_rx.h"))
-    if not force and os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(d) for d in deps):
-        return OUT
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", OUT + ".tmp", *srcs, "-cudart", "static"]
+def build(verbose=False, force=False, out=None, csrc=None, include=None):
+    """out/csrc/include: build another variant (tools/ab_build.py); default = the in-tree library."""
+    OUT_ = out or OUT
+    CSRC_ = csrc or CSRC
+    INC_ = include or os.path.join(os.path.dirname(HERE), "include")
+    srcs = [os.path.join(CSRC_, s) for s in SOURCES]
+    deps = srcs + [os.path.join(CSRC_, f) for f in os.listdir(CSRC_) if f.endswith((".cuh", ".h"))]
+    deps.append(os.path.join(INC_, "kk_rx.h"))
+    if not force and os.path.exists(OUT_) and all(os.path.getmtime(OUT_) >= os.path.getmtime(d) for d in deps):
+        return OUT_
+    flags = [f if f != os.path.join(os.path.dirname(HERE), "include") else INC_ for f in FLAGS]
+    cmd = [NVCC, *ARCH, *flags, "-shared", "-o", OUT_ + ".tmp", *srcs, "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed (%d)" % r.returncode)
-    os.replace(OUT + ".tmp", OUT)
-    with open(os.path.join(HERE, "build.log"), "w") as f:
+    os.replace(OUT_ + ".tmp", OUT_)
+    with open(os.path.join(HERE, "build.log" if out is None else "build_variant.log"), "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    return OUT
+    return OUT_
 
 
 if __name__ == "__main__":

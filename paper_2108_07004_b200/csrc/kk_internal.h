@@ -47,10 +47,10 @@ struct Seg {
   unsigned long long* counts;  // [k][8]
   const float2* taps;      // APPLY: [k][8]
   int64_t n_off;           // APPLY: pattern index of symbol 0 of owner owner_first
+  const int16_t* codes;    // owner o's samples start at codes + o*N (halos readable)
 };
 
 struct ChainArgs {
-  const int16_t* codes;    // sample 0 of owner 0 (halos readable)
   int64_t N;               // buffer_len
   int32_t nseg;
   Seg seg[MAX_SEG];
@@ -71,6 +71,11 @@ struct ChainArgs {
   int64_t P;
   int32_t pat_tma;         // pattern staged by bulk copies (P % 16 == 0)
   DecLut lut;
+  // work distribution: work_ctr == nullptr -> static contiguous ranges per group; else
+  // dynamic grabs from *work_ctr (zeroed before the launch): whole owners of a leading
+  // SEG_X2_TAIL segment first, then guided chunks
+  unsigned long long* work_ctr;
+  unsigned long long* tail_ctr;  // if set: += 1 (release) after every finished SEG_X2_TAIL step
 };
 
 // LMS update-pass look-up table (built on the host):
@@ -106,6 +111,8 @@ struct LmsArgs {
   const float2* w_init;    // [8]
   float2* taps;            // [nchains][8]
   unsigned long long* counts;  // [nbuf][8]
+  const unsigned long long* wait_ctr;  // lane kernel: spin until *wait_ctr >= wait_target (x2 tails ready)
+  unsigned long long wait_target;
 };
 
 struct ApplyArgs {
@@ -132,6 +139,8 @@ cudaError_t chain_setup(int device, int* grid_out);
 cudaError_t lms_setup();
 cudaError_t launch_chain(const ChainArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_lms(const LmsArgs& a, cudaStream_t s);
+cudaError_t launch_lms_lanes(const LmsArgs& a, cudaStream_t s);
+int lms_lanes_ctas(int nchains);
 cudaError_t launch_apply(const ApplyArgs& a, cudaStream_t s);
 
 }  // namespace kk

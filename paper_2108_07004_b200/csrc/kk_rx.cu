@@ -11,6 +11,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -52,6 +53,12 @@ struct kk_rx {
   float2* d_lmslut = nullptr;
   float lms_lcx = 0, lms_lcy = 0, lms_linv = 0;
   uint32_t* d_lut = nullptr;
+  // work counters of the dynamically scheduled chain launches (ring, zeroed per launch)
+  // and the monotone tail-step counter of the async pipeline
+  unsigned long long* d_ctr = nullptr;
+  int ctr_next = 0;
+  unsigned long long tail_done_target = 0;
+  bool dyn_sched = true;
   DecLut lut{};
   uint8_t *d_lab = nullptr, *d_pattern = nullptr;
   // per-chunk scratch (grown on demand to the largest chunk seen)
@@ -342,7 +349,7 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
   void* ptrs[] = {h->d_tw,     h->d_tw512,  h->d_H,      h->d_pts,    h->d_winit,    h->d_lut,
-                  h->d_lab,    h->d_pattern, h->d_lmslut, h->d_tails, h->d_taps,   h->d_counts,   h->d_out,
+                  h->d_lab,    h->d_pattern, h->d_lmslut, h->d_ctr, h->d_tails, h->d_taps,   h->d_counts,   h->d_out,
                   h->d_x2full, h->d_es,     h->d_stage[0], h->d_stage[1]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -581,6 +588,9 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   }
   CKC(chain_setup(dev, &h->grid_chain));
   CKC(lms_setup());
+  CKC(cudaMalloc(&h->d_ctr, 64 * sizeof(unsigned long long)));
+  CKC(cudaMemset(h->d_ctr, 0, 64 * sizeof(unsigned long long)));
+  if (const char* e = std::getenv("KKRX_STATIC_SCHED")) h->dyn_sched = (e[0] == '0');
   CKC(cudaGetLastError());
 #undef CKC
   *out = h;
@@ -611,7 +621,6 @@ static bool is_device_ptr(const void* p) {
 }
 
 static void fill_chain_common(kk_rx_t* h, ChainArgs& ca, const int16_t* codes_dev) {
-  ca.codes = codes_dev;
   ca.N = h->N;
   ca.x2h = h->x2h;
   ca.dc = h->dc;
@@ -623,7 +632,7 @@ static void fill_chain_common(kk_rx_t* h, ChainArgs& ca, const int16_t* codes_de
   ca.tw1024 = h->d_tw;
   ca.tw512 = h->d_tw512;
   ca.Hs = h->d_H;
-  ca.aligned16 = ((uintptr_t)codes_dev % 16) == 0;
+  ca.aligned16 = ((uintptr_t)codes_dev % 16) == 0 && (h->N % 8) == 0;
   ca.n_sym = h->n_sym;
   ca.m = h->m;
   ca.pts = h->d_pts;
@@ -635,6 +644,18 @@ static void fill_chain_common(kk_rx_t* h, ChainArgs& ca, const int16_t* codes_de
 }
 
 static int64_t seg_steps(const Seg& g) { return (int64_t)g.n_own * (g.i_end - g.i_begin); }
+
+// dynamic work distribution for one chain launch: a zeroed counter from the ring
+// (slot 0 is the async pipeline's tail counter)
+static cudaError_t use_dyn(kk_rx_t* h, ChainArgs& ca, cudaStream_t st) {
+  if (!h->dyn_sched) {
+    ca.work_ctr = nullptr;
+    return cudaSuccess;
+  }
+  unsigned long long* c = h->d_ctr + 8 + (h->ctr_next++ % 32);
+  ca.work_ctr = c;
+  return cudaMemsetAsync(c, 0, sizeof(unsigned long long), st);
+}
 
 static kk_status grow(kk_rx_t* h, int64_t nb) {
   if (nb <= h->cap) return KK_OK;
@@ -675,8 +696,8 @@ static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int
     ChainArgs ca{};
     fill_chain_common(h, ca, codes_dev);
     ca.nseg = 2;
-    ca.seg[0] = Seg{-1, 1, h->pre_first, S, SEG_X2_FULL, 0, 0, 0, x2f0, nullptr, nullptr, nullptr, 0};
-    ca.seg[1] = Seg{0, (int32_t)nb, 0, S, SEG_X2_FULL, count_clip, 0, 0, x2f0, nullptr, h->d_counts, nullptr, 0};
+    ca.seg[0] = Seg{-1, 1, h->pre_first, S, SEG_X2_FULL, 0, 0, 0, x2f0, nullptr, nullptr, nullptr, 0, codes_dev};
+    ca.seg[1] = Seg{0, (int32_t)nb, 0, S, SEG_X2_FULL, count_clip, 0, 0, x2f0, nullptr, h->d_counts, nullptr, 0, codes_dev};
     ca.es_dump = es;
     ca.total_steps = seg_steps(ca.seg[0]) + seg_steps(ca.seg[1]);
     CK(launch_chain(ca, h->grid_chain, h->stream));
@@ -689,7 +710,7 @@ static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int
     ChainArgs ca{};
     fill_chain_common(h, ca, codes_dev);
     ca.nseg = 1;
-    ca.seg[0] = Seg{-1, (int32_t)nb, h->pre_first, S, SEG_X2_TAIL, 0, 0, 0, h->d_tails, nullptr, nullptr, nullptr, 0};
+    ca.seg[0] = Seg{-1, (int32_t)nb, h->pre_first, S, SEG_X2_TAIL, 0, 0, 0, h->d_tails, nullptr, nullptr, nullptr, 0, codes_dev};
     ca.total_steps = seg_steps(ca.seg[0]);
     CK(launch_chain(ca, h->grid_chain, h->stream));
     h->last_launches += 1;
@@ -737,8 +758,9 @@ static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int
     ChainArgs ca{};
     fill_chain_common(h, ca, codes_dev);
     ca.nseg = 1;
-    ca.seg[0] = Seg{0, (int32_t)nb, 0, S, SEG_APPLY, 1, 0, 0, nullptr, out_dev, h->d_counts, h->d_taps, n_off0};
+    ca.seg[0] = Seg{0, (int32_t)nb, 0, S, SEG_APPLY, 1, 0, 0, nullptr, out_dev, h->d_counts, h->d_taps, n_off0, codes_dev};
     ca.total_steps = seg_steps(ca.seg[0]);
+    CK(use_dyn(h, ca, h->stream));
     CK(launch_chain(ca, h->grid_chain, h->stream));
   } else {
     ApplyArgs aa{};
