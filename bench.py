@@ -235,7 +235,7 @@ def run_gpu(args):
     span = P + B
     stream_np, off = make_stream(pool, span, left, right, first=0)
     d_stream = torch.from_numpy(stream_np).to(dev)
-    d_out = torch.empty(B * (N // 4), dtype=torch.uint8, device=dev)
+    d_out = [torch.empty(B * (N // 4), dtype=torch.uint8, device=dev) for _ in range(2)]
     cur = torch.cuda.current_stream(dev)
     rx = KKReceiver("CUSTOM" if not cfg.fmt.startswith("QAM") else cfg.fmt, N, cfg.cspr_db, fir, pool.dc_offset,
                     points=pool.points, labels=pool.labels, tone_bin=cfg.tbin, ref_pattern=pool.pattern,
@@ -245,17 +245,19 @@ def run_gpu(args):
         # weak scaling: rank r walks the pool from its own offset
         return (rank * B + step * B * world) % P
 
-    def step_dev(s):
+    # the streaming receiver: kk_rx_submit_batch per step (the LMS update pass of batch
+    # j overlaps the fused chain of batch j-1), kk_rx_sync once after the last step
+    def submit_dev(s):
         b0 = first_buf(s)
         rx.seek(b0)
-        return rx.process_batch(d_stream, off + b0 * N, B, d_out)
+        rx.submit_batch(d_stream, off + b0 * N, B, d_out[s & 1])
 
     for s in range(args.warmup):
-        step_dev(s)
+        submit_dev(s)
+    rx.sync()
     torch.cuda.synchronize(dev)
     rx.set_timing(True)
-    counts = []
-    launches = 0
+    rx.async_launches()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -264,15 +266,32 @@ def run_gpu(args):
     with ClockSampler(local) as clk:
         t0.record(cur)
         for s in range(args.steps):
-            counts += step_dev(args.warmup + s)
-            launches += rx.last_launches()
+            submit_dev(args.warmup + s)
+        counts = rx.sync()
         t1.record(cur)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1)
+    launches = rx.async_launches()
     ktimes = rx.kernel_times()
     rx.set_timing(False)
+
+    # the same steps through the synchronous call (one batch at a time, LMS pass not hidden)
+    def step_sync(s):
+        b0 = first_buf(s)
+        rx.seek(b0)
+        return rx.process_batch(d_stream, off + b0 * N, B, d_out[0])
+    step_sync(0)
+    torch.cuda.synchronize(dev)
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record(cur)
+    for s in range(args.steps):
+        step_sync(s)
+    s1.record(cur)
+    torch.cuda.synchronize(dev)
+    sync_ms = s0.elapsed_time(s1)
     tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
     agg = torch.tensor([sum(c["bit_errors"] for c in counts), sum(c["bits"] for c in counts),
                         sum(c["sym_errors"] for c in counts), sum(c["symbols"] for c in counts)],
@@ -288,14 +307,15 @@ def run_gpu(args):
     e2e = None
     if not args.no_e2e:
         h_stream = torch.from_numpy(stream_np).pin_memory()
-        h_out = torch.empty(B * (N // 4), dtype=torch.uint8).pin_memory()
+        h_out = [torch.empty(B * (N // 4), dtype=torch.uint8).pin_memory() for _ in range(2)]
 
-        def step_host(s):
+        def submit_host(s):
             b0 = first_buf(s)
             rx.seek(b0)
-            return rx.process_batch(h_stream, off + b0 * N, B, h_out)
+            rx.submit_batch(h_stream, off + b0 * N, B, h_out[s & 1])
 
-        step_host(0)
+        submit_host(0)
+        rx.sync()
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
@@ -303,7 +323,8 @@ def run_gpu(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(cur)
         for s in range(args.steps):
-            step_host(s)
+            submit_host(s)
+        rx.sync()
         e1.record(cur)
         torch.cuda.synchronize(dev)
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -323,11 +344,12 @@ def run_gpu(args):
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     ch_ms, ch_n = ktimes["chain"]
+    if ch_n == 0:
+        raise RuntimeError("no chain kernel timing recorded")
     ch_avg_ms = ch_ms / max(ch_n, 1)
     achieved_tf = FLOP_PER_SA_KERNEL * B * N / (ch_avg_ms / 1e3) / 1e12
     traffic = profile_traffic()
     step_ms = ms_max / args.steps
-    tail_avg = ktimes["x2_pass"][0] / max(ktimes["x2_pass"][1], 1)
     lms_avg = ktimes["lms"][0] / max(ktimes["lms"][1], 1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -351,7 +373,11 @@ def run_gpu(args):
                      "hbm_algorithmic_bytes_per_launch": HBM_BYTES_PER_SA * B * N,
                      "hbm_achieved_gbs": HBM_BYTES_PER_SA * B * N / (ch_avg_ms / 1e3) / 1e9,
                      "peak_basis": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (derived, DESIGN.md)"},
-        "kernel_ms_per_step": {"x2_tails": tail_avg, "lms": lms_avg, "chain": ch_avg_ms},
+        "kernel_ms_per_step": {"chain": ch_avg_ms, "lms_overlapped": lms_avg},
+        "pipeline": ("kk_rx_submit_batch per step + one kk_rx_sync: the LMS update pass of batch j (one SM, "
+                     "lane-per-chain) overlaps the fused chain of batch j-1, whose launch also computes batch j's "
+                     "update-pass x2 tails first"),
+        "sync_value": samples_total / world / (sync_ms / 1e3) / 1e9 * world,
         "errors": {"bit_errors": int(agg[0]), "bits": int(agg[1]), "ber": int(agg[0]) / max(int(agg[1]), 1)},
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -138,6 +138,30 @@ kk_status kk_rx_process(kk_rx_t *h, const int16_t *buffer, uint8_t *out_symbols,
 kk_status kk_rx_process_batch(kk_rx_t *h, const int16_t *first, int64_t nbuf, uint8_t *out_symbols,
                               kk_rx_counts *out_per_buf);
 
+/* Asynchronous submission (the streaming receiver).
+ * Enqueues nbuf consecutive buffers starting at `first` (contiguous stream, halos
+ * readable; device memory, or host memory staged through the handle's copy stream)
+ * and returns without waiting.  The library keeps two batches in flight: the LMS
+ * update pass of batch j (one SM) runs concurrently with the fused chain of batch
+ * j-1, and that chain launch also computes batch j's update-pass x2 tails.  The
+ * chain of the newest batch is launched by the next submit or by kk_rx_sync.
+ * Results equal kk_rx_process_batch on the same buffers bit for bit.
+ * `first` (and the halos) must stay valid and unmodified until kk_rx_sync returns;
+ * input written by the caller on the handle's cuda_stream before the call is
+ * honoured (stream order).  out_symbols: nbuf*buffer_len/4 bytes (device or host)
+ * or NULL; valid after kk_rx_sync.  Advances the stream position by nbuf.
+ * Errors: KK_EUNSUPPORTED with sub_block < buffer_len/4 or debug dumps; KK_EINVAL
+ * for bad arguments or nbuf > 4096. */
+kk_status kk_rx_submit_batch(kk_rx_t *h, const int16_t *first, int64_t nbuf, uint8_t *out_symbols);
+
+/* Finish every submitted batch and return their per-buffer counters in submission
+ * order: up to max_out structs to out_per_buf (may be NULL), the total count to
+ * *n_out (may be NULL).  Blocks until all outputs are valid. */
+kk_status kk_rx_sync(kk_rx_t *h, kk_rx_counts *out_per_buf, int64_t max_out, int64_t *n_out);
+
+/* Kernel launches issued by submit/sync since the previous call of this function. */
+int64_t kk_rx_async_launches(kk_rx_t *h);
+
 /* Set the stream index of the next buffer (pattern offset = ref_offset +
  * index*buffer_len/4 mod ref_len).  Default after create: 0. */
 kk_status kk_rx_seek(kk_rx_t *h, int64_t buffer_index);

@@ -34,6 +34,26 @@ kk_status fail(kk_status s, const std::string& msg) {
 }
 }  // namespace
 
+// One in-flight batch of the asynchronous pipeline (kk_rx_submit_batch).
+struct AsyncSlot {
+  int64_t cap = 0;                          // buffers the scratch below holds
+  float2* tails = nullptr;                  // [(cap + 1) * x2h + 64] update-pass x2 tails
+  float2* taps = nullptr;                   // [cap][8]
+  unsigned long long* d_counts = nullptr;   // [cap][8]
+  unsigned long long* h_counts = nullptr;   // pinned [cap][8]
+  uint8_t* d_out = nullptr;                 // labels staging (host or NULL output) [cap * n_sym]
+  int16_t* d_stage = nullptr;               // host input staging [left + cap*N + right]
+  int64_t stage_cap = 0;
+  int64_t nb = 0, index = 0, n_off0 = 0;
+  const int16_t* codes = nullptr;           // device samples of buffer 0 of the batch
+  uint8_t* out_dev = nullptr;               // where the chain writes labels
+  uint8_t* out_host = nullptr;              // host destination (D2H after the chain) or NULL
+  cudaEvent_t ev_lms = nullptr, ev_done = nullptr, ev_h2d = nullptr;
+  cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};  // timing: LMS start/end, chain start/end
+  bool timed_lms = false, timed_chain = false;
+  int state = 0;                            // 0 free, 1 LMS issued + chain deferred, 2 chain issued
+};
+
 struct kk_rx {
   int device = 0;
   int64_t N = 0, n_sym = 0, L = 0;
@@ -59,6 +79,16 @@ struct kk_rx {
   int ctr_next = 0;
   unsigned long long tail_done_target = 0;
   bool dyn_sched = true;
+  // asynchronous pipeline
+  static constexpr int NSLOT = 3;         // batches in flight: LMS(j) | chain(j-1) queued | chain(j-2) running
+  AsyncSlot aslot[NSLOT];
+  int a_next = 0, a_deferred = -1;
+  int a_order[NSLOT] = {-1, -1, -1};       // slots with an issued chain, oldest first
+  int a_norder = 0;
+  std::vector<kk_rx_counts> a_counts;      // harvested per-buffer counters since the last sync
+  cudaStream_t lms_stream = nullptr, h2d_stream = nullptr;
+  cudaEvent_t ev_in = nullptr;
+  int64_t a_launches = 0;
   DecLut lut{};
   uint8_t *d_lab = nullptr, *d_pattern = nullptr;
   // per-chunk scratch (grown on demand to the largest chunk seen)
@@ -354,6 +384,19 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_counts) cudaFreeHost(h->h_counts);
+  if (h->lms_stream) cudaStreamSynchronize(h->lms_stream);
+  if (h->h2d_stream) cudaStreamSynchronize(h->h2d_stream);
+  for (AsyncSlot& a : h->aslot) {
+    void* ap[] = {a.tails, a.taps, a.d_counts, a.d_out, a.d_stage};
+    for (void* q : ap)
+      if (q) cudaFree(q);
+    if (a.h_counts) cudaFreeHost(a.h_counts);
+    for (cudaEvent_t e : {a.ev_lms, a.ev_done, a.ev_h2d, a.ev_t[0], a.ev_t[1], a.ev_t[2], a.ev_t[3]})
+      if (e) cudaEventDestroy(e);
+  }
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->lms_stream) cudaStreamDestroy(h->lms_stream);
+  if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
   for (int i = 0; i < 2; ++i) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_used[i]) cudaEventDestroy(h->ev_used[i]);
@@ -902,6 +945,281 @@ kk_status kk_rx_process_batch(kk_rx_t* h, const int16_t* first, int64_t nbuf, ui
   return KK_OK;
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Asynchronous pipeline: batch j's LMS update pass
+// (one SM, lane-per-chain kernel, side stream) runs concurrently with the fused
+// chain of batch j-1, whose launch also computes batch j's x2 tails first (the LMS
+// kernel waits on their completion counter).  The chain of the newest batch is
+// deferred to the next submit or to kk_rx_sync.
+// ---------------------------------------------------------------------------
+static kk_status slot_reserve(kk_rx_t* h, AsyncSlot& a, int64_t nb, bool host_in) {
+  if (!a.ev_lms) {
+    CK(cudaEventCreateWithFlags(&a.ev_lms, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&a.ev_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&a.ev_h2d, cudaEventDisableTiming));
+    for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&a.ev_t[k]));
+  }
+  if (nb > a.cap) {
+    void* ap[] = {a.tails, a.taps, a.d_counts, a.d_out};
+    for (void* q : ap)
+      if (q) cudaFree(q);
+    if (a.h_counts) cudaFreeHost(a.h_counts);
+    a.tails = nullptr;
+    a.taps = nullptr;
+    a.d_counts = nullptr;
+    a.d_out = nullptr;
+    a.h_counts = nullptr;
+    a.cap = 0;
+    CK(cudaMalloc(&a.tails, (size_t)((nb + 1) * h->x2h + 64) * sizeof(float2)));
+    CK(cudaMalloc(&a.taps, (size_t)nb * 8 * sizeof(float2)));
+    CK(cudaMalloc(&a.d_counts, (size_t)nb * 8 * sizeof(unsigned long long)));
+    CK(cudaMalloc(&a.d_out, (size_t)nb * h->n_sym));
+    CK(cudaMallocHost(&a.h_counts, (size_t)nb * 8 * sizeof(unsigned long long)));
+    a.cap = nb;
+  }
+  if (host_in && nb > a.stage_cap) {
+    if (a.d_stage) cudaFree(a.d_stage);
+    a.d_stage = nullptr;
+    a.stage_cap = 0;
+    CK(cudaMalloc(&a.d_stage, (size_t)(h->left + nb * h->N + h->right) * sizeof(int16_t)));
+    a.stage_cap = nb;
+  }
+  return KK_OK;
+}
+
+static void slot_harvest(kk_rx_t* h, AsyncSlot& a) {
+  // per-kernel device times of this batch (kk_rx_set_timing): [1] LMS pass, [2] chain launch
+  float ms = 0.f;
+  if (a.timed_lms && cudaEventElapsedTime(&ms, a.ev_t[0], a.ev_t[1]) == cudaSuccess) {
+    h->kernel_ms[1] += ms;
+    h->kernel_n[1] += 1;
+  }
+  if (a.timed_chain && cudaEventElapsedTime(&ms, a.ev_t[2], a.ev_t[3]) == cudaSuccess) {
+    h->kernel_ms[2] += ms;
+    h->kernel_n[2] += 1;
+  }
+  a.timed_lms = a.timed_chain = false;
+  for (int64_t b = 0; b < a.nb; ++b) {
+    const unsigned long long* c = a.h_counts + 8 * b;
+    kk_rx_counts r{};
+    r.bit_errors = c[C_BITERR];
+    r.sym_errors = c[C_SYMERR];
+    r.bits = h->has_pattern ? (uint64_t)h->n_sym * h->bits_per : 0;
+    r.symbols = (uint64_t)h->n_sym;
+    r.clipped_samples = c[C_CLIP];
+    r.gated_updates = c[C_GATED];
+    r.flags = (uint32_t)c[C_FLAGS];
+    h->a_counts.push_back(r);
+    h->totals.bit_errors += r.bit_errors;
+    h->totals.sym_errors += r.sym_errors;
+    h->totals.bits += r.bits;
+    h->totals.symbols += r.symbols;
+    h->totals.clipped_samples += r.clipped_samples;
+    h->totals.gated_updates += r.gated_updates;
+    h->totals.flags |= r.flags;
+  }
+  a.state = 0;
+}
+
+// the fused chain of slot p (APPLY), optionally preceded in the same launch by the
+// x2 tails of slot t's batch (a leading SEG_X2_TAIL segment, published via the counter)
+static kk_status issue_chain(kk_rx_t* h, int p, int t) {
+  AsyncSlot& ap = h->aslot[p];
+  CK(cudaStreamWaitEvent(h->stream, ap.ev_lms, 0));
+  ChainArgs ca{};
+  fill_chain_common(h, ca, ap.codes);
+  const int S = h->steps_per_buf;
+  int ns = 0;
+  int grid = h->grid_chain;
+  if (t >= 0) {
+    AsyncSlot& at = h->aslot[t];
+    ca.seg[ns++] = Seg{-1, (int32_t)at.nb, h->pre_first, S, SEG_X2_TAIL, 0, 0, 0, at.tails, nullptr, nullptr,
+                       nullptr, 0, at.codes};
+    ca.tail_ctr = h->d_ctr;
+    ca.aligned16 = ca.aligned16 && ((uintptr_t)at.codes % 16) == 0;
+    grid -= lms_lanes_ctas((int)at.nb);  // leave SMs to the concurrent LMS pass
+  }
+  ca.seg[ns++] = Seg{0, (int32_t)ap.nb, 0, S, SEG_APPLY, 1, 0, 0, nullptr, ap.out_dev, ap.d_counts, ap.taps, ap.n_off0,
+                     ap.codes};
+  ca.nseg = ns;
+  ca.total_steps = 0;
+  for (int k = 0; k < ns; ++k) ca.total_steps += seg_steps(ca.seg[k]);
+  {
+    const bool d = h->dyn_sched;
+    h->dyn_sched = true;  // the tail segment must be grabbed first
+    cudaError_t e = use_dyn(h, ca, h->stream);
+    h->dyn_sched = d;
+    CK(e);
+  }
+  if (h->timing) CK(cudaEventRecord(ap.ev_t[2], h->stream));
+  CK(launch_chain(ca, grid, h->stream));
+  if (h->timing) CK(cudaEventRecord(ap.ev_t[3], h->stream));
+  ap.timed_chain = h->timing;
+  h->a_launches += 1;
+  if (ap.out_host)
+    CK(cudaMemcpyAsync(ap.out_host, ap.out_dev, (size_t)ap.nb * h->n_sym, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(ap.h_counts, ap.d_counts, (size_t)ap.nb * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaEventRecord(ap.ev_done, h->stream));
+  ap.state = 2;
+  h->a_order[h->a_norder++] = p;
+  return KK_OK;
+}
+
+extern "C" kk_status kk_rx_submit_batch(kk_rx_t* h, const int16_t* first, int64_t nbuf, uint8_t* out_symbols) {
+  if (!h) return fail(KK_EINVAL, "null handle");
+  if (h->sticky != KK_OK) return fail(KK_ESTATE, "handle is in a failed state (previous CUDA error)");
+  if (!first || nbuf <= 0) return fail(KK_EINVAL, "need a buffer pointer and nbuf > 0");
+  if (h->nsub != 1) return fail(KK_EUNSUPPORTED, "kk_rx_submit_batch needs sub_block == buffer_len/4");
+  if (h->dump) return fail(KK_EUNSUPPORTED, "kk_rx_submit_batch does not support debug dumps");
+  if (nbuf > 4096) return fail(KK_EINVAL, "nbuf > 4096 per submission");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  CK(cudaSetDevice(h->device));
+  struct Restore {
+    int d;
+    ~Restore() { cudaSetDevice(d); }
+  } restore{cur};
+  if (!h->lms_stream) {
+    CK(cudaStreamCreateWithFlags(&h->lms_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+  }
+  const bool in_dev = is_device_ptr(first);
+  const bool out_dev = out_symbols ? is_device_ptr(out_symbols) : false;
+  const int s = h->a_next;
+  AsyncSlot& a = h->aslot[s];
+  if (a.state == 2) {  // the chain of NSLOT submissions ago (normally finished): wait and harvest
+    CK(cudaEventSynchronize(a.ev_done));
+    if (h->a_norder > 0 && h->a_order[0] == s) {
+      slot_harvest(h, a);
+      for (int k = 1; k < h->a_norder; ++k) h->a_order[k - 1] = h->a_order[k];
+      h->a_norder -= 1;
+    }
+  }
+  if (a.state != 0) return fail(KK_ESTATE, "async slot busy");
+  kk_status st = slot_reserve(h, a, nbuf, !in_dev);
+  if (st != KK_OK) return st;
+  a.nb = nbuf;
+  a.index = h->stream_index;
+  const int64_t Pp = h->P;
+  int64_t n_off0 = h->has_pattern ? ((h->ref_offset + (h->stream_index % Pp) * (h->n_sym % Pp)) % Pp) : 0;
+  if (n_off0 < 0) n_off0 += Pp;
+  a.n_off0 = n_off0;
+  a.out_dev = (out_symbols && out_dev) ? out_symbols : a.d_out;
+  a.out_host = (out_symbols && !out_dev) ? out_symbols : nullptr;
+  CK(cudaEventRecord(h->ev_in, h->stream));  // the caller's prior work on its stream
+  CK(cudaStreamWaitEvent(h->lms_stream, h->ev_in, 0));
+  if (in_dev) {
+    a.codes = first;
+  } else {
+    // host input: pinned (or pageable) -> slot staging on the copy stream
+    CK(cudaStreamWaitEvent(h->h2d_stream, h->ev_in, 0));
+    CK(cudaMemcpyAsync(a.d_stage, first - h->left, (size_t)(h->left + nbuf * h->N + h->right) * sizeof(int16_t),
+                       cudaMemcpyHostToDevice, h->h2d_stream));
+    CK(cudaEventRecord(a.ev_h2d, h->h2d_stream));
+    CK(cudaStreamWaitEvent(h->lms_stream, a.ev_h2d, 0));
+    a.codes = a.d_stage + h->left;
+  }
+  CK(cudaMemsetAsync(a.d_counts, 0, (size_t)nbuf * 8 * sizeof(unsigned long long), h->lms_stream));
+  LmsArgs la{};
+  la.lut = h->d_lmslut;
+  la.lcx = h->lms_lcx;
+  la.lcy = h->lms_lcy;
+  la.linv = h->lms_linv;
+  la.x2_b0 = a.tails + h->x2h;
+  la.x2_stride = h->x2h;
+  la.n_sym = h->n_sym;
+  la.L = h->L;
+  la.nsub = 1;
+  la.nchains = (int32_t)nbuf;
+  la.K = h->K;
+  la.mu = h->mu;
+  la.inv_tau = h->tau > 0.f ? 1.0f / h->tau : 0.f;
+  la.mode = h->mode;
+  la.m = h->m;
+  la.pts = h->d_pts;
+  la.pattern = h->has_pattern ? h->d_pattern : nullptr;
+  la.P = Pp;
+  la.n_off0 = n_off0;
+  la.w_init = h->d_winit;
+  la.taps = a.taps;
+  la.counts = a.d_counts;
+  const int p = h->a_deferred;
+  if (p < 0) {
+    // pipeline empty: the tails of this batch by their own launch, then the update pass
+    ChainArgs ca{};
+    fill_chain_common(h, ca, a.codes);
+    ca.nseg = 1;
+    ca.seg[0] = Seg{-1, (int32_t)nbuf, h->pre_first, h->steps_per_buf, SEG_X2_TAIL, 0, 0, 0, a.tails,
+                    nullptr, nullptr, nullptr, 0, a.codes};
+    ca.total_steps = seg_steps(ca.seg[0]);
+    CK(launch_chain(ca, h->grid_chain, h->lms_stream));
+    // nothing else runs yet: the one-warp-per-chain kernel (lowest latency, many SMs)
+    if (h->timing) CK(cudaEventRecord(a.ev_t[0], h->lms_stream));
+    CK(launch_lms(la, h->lms_stream));
+    if (h->timing) CK(cudaEventRecord(a.ev_t[1], h->lms_stream));
+    h->a_launches += 2;
+  } else {
+    // this batch's update pass waits for its tails, computed first by the chain launch of batch p
+    h->tail_done_target += (unsigned long long)nbuf * (unsigned long long)h->pre_steps;
+    la.wait_ctr = h->d_ctr;
+    la.wait_target = h->tail_done_target;
+    if (h->timing) CK(cudaEventRecord(a.ev_t[0], h->lms_stream));
+    CK(launch_lms_lanes(la, h->lms_stream));
+    if (h->timing) CK(cudaEventRecord(a.ev_t[1], h->lms_stream));
+    a.timed_lms = h->timing;
+    h->a_launches += 1;
+  }
+  CK(cudaEventRecord(a.ev_lms, h->lms_stream));
+  a.state = 1;
+  if (p >= 0) {
+    st = issue_chain(h, p, s);
+    if (st != KK_OK) return st;
+  }
+  h->a_deferred = s;
+  h->a_next = (s + 1) % kk_rx::NSLOT;
+  h->stream_index += nbuf;
+  return KK_OK;
+}
+
+extern "C" kk_status kk_rx_sync(kk_rx_t* h, kk_rx_counts* out_per_buf, int64_t max_out, int64_t* n_out) {
+  if (!h) return fail(KK_EINVAL, "null handle");
+  if (h->sticky != KK_OK) return fail(KK_ESTATE, "handle is in a failed state (previous CUDA error)");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  CK(cudaSetDevice(h->device));
+  struct Restore {
+    int d;
+    ~Restore() { cudaSetDevice(d); }
+  } restore{cur};
+  if (h->a_deferred >= 0) {
+    kk_status st = issue_chain(h, h->a_deferred, -1);
+    if (st != KK_OK) return st;
+    h->a_deferred = -1;
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  if (h->lms_stream) CK(cudaStreamSynchronize(h->lms_stream));
+  for (int k = 0; k < h->a_norder; ++k) slot_harvest(h, h->aslot[h->a_order[k]]);
+  h->a_norder = 0;
+  const int64_t n = (int64_t)h->a_counts.size();
+  if (out_per_buf)
+    for (int64_t i = 0; i < n && i < max_out; ++i) out_per_buf[i] = h->a_counts[i];
+  if (n_out) *n_out = n;
+  h->a_counts.clear();
+  return KK_OK;
+}
+
+extern "C" int64_t kk_rx_async_launches(kk_rx_t* h) {
+  if (!h) return 0;
+  const int64_t n = h->a_launches;
+  h->a_launches = 0;
+  return n;
+}
+
+extern "C" {
 kk_status kk_rx_process(kk_rx_t* h, const int16_t* buffer, uint8_t* out_symbols, kk_rx_counts* out_errors) {
   return kk_rx_process_batch(h, buffer, 1, out_symbols, out_errors);
 }

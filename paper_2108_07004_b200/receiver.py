@@ -113,6 +113,27 @@ class KKReceiver:
               "kk_rx_process_batch")
         return [c.as_dict() for c in cnt]
 
+    def submit_batch(self, stream, offset, nbuf, out=None):
+        """Asynchronous kk_rx_submit_batch: enqueue nbuf buffers (see process_batch for
+        the arguments); outputs and counters become valid at sync()."""
+        base, es = _ptr(stream)
+        assert es == 2
+        optr = None
+        if out is not None:
+            optr, _ = _ptr(out)
+        check(self._lib.kk_rx_submit_batch(self.h, C.c_void_p(base + 2 * int(offset)), int(nbuf),
+                                           C.c_void_p(optr) if optr is not None else None), "kk_rx_submit_batch")
+
+    def sync(self, max_out=1 << 16):
+        """kk_rx_sync: wait for every submitted batch; per-buffer counter dicts in order."""
+        cnt = (KKCounts * int(max_out))()
+        n = C.c_int64()
+        check(self._lib.kk_rx_sync(self.h, cnt, int(max_out), C.byref(n)), "kk_rx_sync")
+        return [cnt[i].as_dict() for i in range(min(n.value, max_out))]
+
+    def async_launches(self):
+        return int(self._lib.kk_rx_async_launches(self.h))
+
     def process(self, stream, offset, out=None):
         return self.process_batch(stream, offset, 1, out)[0]
 

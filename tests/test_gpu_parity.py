@@ -240,3 +240,93 @@ def test_empty_and_invalid_calls():
         g["rx"].process_batch(torch.from_numpy(g["stream"]).cuda(), g["off"], 0)
     with pytest.raises(KKError):
         g["rx"].taps(5)
+
+
+def test_async_pipeline_equals_process_batch():
+    """kk_rx_submit_batch / kk_rx_sync (LMS pass of batch j concurrent with the chain
+    of batch j-1, tails computed inside the previous chain launch) give labels and
+    counters bit-identical to kk_rx_process_batch, for ragged submission sizes,
+    device and pinned-host buffers, and a pipeline restarted after a sync."""
+    _require_gpu()
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    name = "C2_n16"
+    cfg = configs.get(name).link
+    pool = make_pool(cfg, 6)
+    fir = _fir(name)
+    left, right = halo_for(cfg.buffer_len)
+    nbuf = 6
+    stream, off = make_stream(pool, nbuf, left, right)
+    n = cfg.buffer_len
+    n_sym = n // 4
+
+    def rx():
+        return KKReceiver(cfg.fmt, n, cfg.cspr_db, fir, pool.dc_offset, tone_bin=cfg.tbin, ref_pattern=pool.pattern,
+                          max_batch=nbuf)
+    ref = rx()
+    src = torch.from_numpy(stream).cuda()
+    out_ref = torch.empty(nbuf * n_sym, dtype=torch.uint8, device="cuda")
+    c_ref = ref.process_batch(src, off, nbuf, out_ref)
+    lab_ref = out_ref.cpu().numpy()
+
+    for host in (False, True):
+        r = rx()
+        s = torch.from_numpy(stream).pin_memory() if host else src
+        out = (torch.empty(nbuf * n_sym, dtype=torch.uint8).pin_memory() if host else
+               torch.empty(nbuf * n_sym, dtype=torch.uint8, device="cuda"))
+        for rnd in range(2):  # second round: pipeline restarted after sync
+            out.zero_()
+            r.seek(0)
+            b0 = 0
+            for k in (2, 1, 3):
+                r.submit_batch(s, off + b0 * n, k, out[b0 * n_sym:(b0 + k) * n_sym])
+                b0 += k
+            assert r.async_launches() > 0
+            c = r.sync()
+            torch.cuda.synchronize()
+            assert c == c_ref, (host, rnd)
+            assert np.array_equal(out.cpu().numpy(), lab_ref), (host, rnd)
+        r.close()
+    ref.close()
+
+
+def test_async_full_size_bench_config():
+    """The bench's launch configuration: C5 (GS-128) at full size, 64-buffer
+    submissions through the async pipeline, device-resident.  Two submissions equal
+    one process_batch call bit for bit, and one buffer of the batch is checked
+    against the float64 oracle."""
+    _require_gpu()
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    name = "C5"
+    cfg = configs.get(name).link
+    pool = make_pool(cfg, 16)
+    fir = _fir(name)
+    n = cfg.buffer_len
+    n_sym = n // 4
+    B = 64
+    left, right = halo_for(n)
+    stream, off = make_stream(pool, 2 * B, left, right)
+    src = torch.from_numpy(stream).cuda()
+    kw = dict(points=pool.points, labels=pool.labels, tone_bin=cfg.tbin, ref_pattern=pool.pattern, max_batch=B)
+    a = KKReceiver("CUSTOM", n, cfg.cspr_db, fir, pool.dc_offset, **kw)
+    out_a = torch.empty(2 * B * n_sym, dtype=torch.uint8, device="cuda")
+    a.submit_batch(src, off, B, out_a[:B * n_sym])
+    a.submit_batch(src, off + B * n, B, out_a[B * n_sym:])
+    ca = a.sync()
+    b = KKReceiver("CUSTOM", n, cfg.cspr_db, fir, pool.dc_offset, **kw)
+    out_b = torch.empty(2 * B * n_sym, dtype=torch.uint8, device="cuda")
+    cb = b.process_batch(src, off, 2 * B, out_b)
+    assert ca == cb
+    lab = out_a.cpu().numpy()
+    assert np.array_equal(lab, out_b.cpu().numpy())
+    # one buffer (index 37 of the first submission) against the oracle
+    k = 37
+    o = _oracle(stream, off, k, cfg, pool, fir, left, right)
+    inv = np.argsort(pool.labels)
+    dec = inv[lab[k * n_sym:(k + 1) * n_sym].astype(np.int64)]
+    ok = o["margin"] >= EXEMPT
+    assert np.all(dec[ok] == o["decisions"][ok])
+    ro = O.count_errors(o["decisions"][ok], o["ref"][ok], pool.labels)
+    rg = O.count_errors(dec[ok], o["ref"][ok], pool.labels)
+    assert ro == rg
+    a.close()
+    b.close()
