@@ -50,34 +50,6 @@ struct Seg {
   const int16_t* codes;    // owner o's samples start at codes + o*N (halos readable)
 };
 
-struct ChainArgs {
-  int64_t N;               // buffer_len
-  int32_t nseg;
-  Seg seg[MAX_SEG];
-  int64_t total_steps;
-  int64_t x2h;             // tail length (x2 samples) = 2K + 64
-  float dc, vmin, a_hat, invN;
-  uint32_t tb_mod, s32;    // tone_bin mod N, (tb*32) mod N
-  const float2* tw1024;    // [32*32] e^{-2 pi i r l / 1024}
-  const float2* tw512;     // [16*32] e^{-2 pi i r l / 512}
-  const float2* Hs;        // [1024] DFT of the tone-shifted h, / 1024 (reading R5 + downconversion)
-  float2* es_dump;         // debug: E_s of owners >= 0 of FULL segments, [owner*N + p], or nullptr
-  int aligned16;
-  int64_t n_sym;
-  int32_t m;
-  const float2* pts;       // [m]
-  const uint8_t* labels;   // [m]
-  const uint8_t* pattern;  // [P] or nullptr
-  int64_t P;
-  int32_t pat_tma;         // pattern staged by bulk copies (P % 16 == 0)
-  DecLut lut;
-  // work distribution: work_ctr == nullptr -> static contiguous ranges per group; else
-  // dynamic grabs from *work_ctr (zeroed before the launch): whole owners of a leading
-  // SEG_X2_TAIL segment first, then guided chunks
-  unsigned long long* work_ctr;
-  unsigned long long* tail_ctr;  // if set: += 1 (release) after every finished SEG_X2_TAIL step
-};
-
 // LMS update-pass look-up table (built on the host):
 // G x G cells (G a power of two) over the constellation's bounding box (+2 d_min).
 // Entry of cell (cx, cy) = float2:
@@ -113,6 +85,38 @@ struct LmsArgs {
   unsigned long long* counts;  // [nbuf][8]
   const unsigned long long* wait_ctr;  // lane kernel: spin until *wait_ctr >= wait_target (x2 tails ready)
   unsigned long long wait_target;
+};
+
+struct ChainArgs {
+  int64_t N;               // buffer_len
+  int32_t nseg;
+  Seg seg[MAX_SEG];
+  int64_t total_steps;
+  int64_t x2h;             // tail length (x2 samples) = 2K + 64
+  float dc, vmin, a_hat, invN;
+  uint32_t tb_mod, s32;    // tone_bin mod N, (tb*32) mod N
+  const float2* tw1024;    // [32*32] e^{-2 pi i r l / 1024}
+  const float2* tw512;     // [16*32] e^{-2 pi i r l / 512}
+  const float2* Hs;        // [1024] DFT of the tone-shifted h, / 1024 (reading R5 + downconversion)
+  float2* es_dump;         // debug: E_s of owners >= 0 of FULL segments, [owner*N + p], or nullptr
+  int aligned16;
+  int64_t n_sym;
+  int32_t m;
+  const float2* pts;       // [m]
+  const uint8_t* labels;   // [m]
+  const uint8_t* pattern;  // [P] or nullptr
+  int64_t P;
+  int32_t pat_tma;         // pattern staged by bulk copies (P % 16 == 0)
+  DecLut lut;
+  // work distribution: work_ctr == nullptr -> static contiguous ranges per group; else
+  // dynamic grabs from *work_ctr (zeroed before the launch): whole owners of a leading
+  // SEG_X2_TAIL segment first, then guided chunks
+  unsigned long long* work_ctr;
+  unsigned long long* tail_ctr;  // if set: += 1 (release) after every finished SEG_X2_TAIL step
+  // the LMS update pass of the next batch as extra CTAs of this launch (the last lms_ctas
+  // blocks; lane-per-chain body, waits on tail_ctr for the tails this launch computes)
+  int32_t lms_ctas, lms_mode;
+  LmsArgs lms;
 };
 
 struct ApplyArgs {

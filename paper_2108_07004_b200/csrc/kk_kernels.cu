@@ -20,6 +20,12 @@
 
 namespace kk {
 
+// compile-time phase tag of unrolled loop bodies
+template <int Q>
+struct Phase {
+  static constexpr int value = Q;
+};
+
 // one CTA per SM = NGROUP independent 4-warp groups (each the former 128-thread CTA,
 // synchronised by its own named barrier) sharing one copy of the read-only tables
 constexpr size_t SMEM_TW = 1024 * sizeof(float2);     // 1024-pt twiddles
@@ -34,6 +40,7 @@ constexpr size_t SMEM_PAT = 832;                 // pattern bytes of one step (7
 constexpr size_t SMEM_GROUP = SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT + 64 + 16;  // + factored WL taps + mbarriers
 constexpr size_t CHAIN_SMEM = SMEM_SHARED + NGROUP * SMEM_GROUP;
 static_assert(SMEM_GROUP % 16 == 0 && SMEM_SHARED % 16 == 0, "16-B aligned regions");
+static_assert(LMS_LUT_G * LMS_LUT_G * 8 + 129 * 8 <= SMEM_SHARED + NGROUP * SMEM_GROUP, "LMS CTAs fit the chain smem");
 static_assert(WARM * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-up codes + tile must fit the x2 window");
 static_assert(TILE * sizeof(float) <= EQ_KEEP * sizeof(float2), "transpose tile must fit an EQ stride of ebuf");
 
@@ -214,6 +221,231 @@ __device__ __forceinline__ StepPos decode_step(const ChainArgs& a, int64_t g) {
   return r;
 }
 
+constexpr size_t LMS_LUT_BYTES = (size_t)LMS_LUT_G * LMS_LUT_G * sizeof(float2);
+
+// ---------------------------------------------------------------------------
+// Kernel 2b: LMS update pass with one LANE per chain (up to 512 chains per CTA,
+// all sharing one copy of the LMS table).  Same arithmetic and step order as
+// kk_lms_kernel; a warp's instruction stream serves 32 chains, so the whole
+// update pass of a batch occupies a single SM and runs concurrently with the
+// fused chain kernel of the previous batch (kk_rx_submit_batch pipeline).  The
+// x2 samples stream from L2 through a 16-register ring per lane, prefetched five
+// steps ahead.  Optionally spins until the chain kernel has published the x2
+// tails it reads (wait_ctr).
+// ---------------------------------------------------------------------------
+constexpr int LMSL_MAXW = 16;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// body shared by the standalone kernel (compile-time MODE) and the LMS CTAs of a
+// fused chain launch (kk_chain_kernel, runtime mode); smem: [LUT 128 KB][s_pts 129]
+// MODE: 0 DD soft gate, 1 PILOT (known pattern), 2 DD hard (gamma = 1)
+__device__ __forceinline__ void lms_lanes_body(const LmsArgs& a, unsigned char* lmsl_smem, int blk, const int MODE) {
+  float2* s_pts = reinterpret_cast<float2*>(lmsl_smem + LMS_LUT_BYTES);
+  const float2* s_lut = reinterpret_cast<const float2*>(lmsl_smem);
+  const float INF = __int_as_float(0x7f800000);
+  if (MODE != 1) {
+    const float4* src = reinterpret_cast<const float4*>(a.lut);
+    float4* dst = reinterpret_cast<float4*>(lmsl_smem);
+    for (int i = threadIdx.x; i < LMS_LUT_G * LMS_LUT_G / 2; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  for (int i = threadIdx.x; i < 129; i += blockDim.x) s_pts[i] = (i < a.m) ? a.pts[i] : make_float2(INF, INF);
+  __syncthreads();
+  if (a.wait_ctr) {
+    if ((threadIdx.x & 31) == 0)
+      while (ld_acquire_u64(a.wait_ctr) < a.wait_target) __nanosleep(200);
+    __syncwarp();
+  }
+  const int c = blk * blockDim.x + threadIdx.x;
+  const bool valid = c < a.nchains;
+  const int cc = valid ? c : a.nchains - 1;  // idle lanes replay the last chain, results dropped
+  const int b = cc / a.nsub, sblk = cc - b * a.nsub;
+  const int64_t n0l = (int64_t)sblk * a.L - a.K;
+  const int64_t n0 = (int64_t)b * a.n_sym + n0l;
+  const float2* xw = a.x2_b0 + (int64_t)b * a.x2_stride + 2 * n0l - 4;  // W[i] = xw[i] (= x2[2 n0l - 4 + i])
+  float A[4], B[4], C[4], D[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 w = a.w_init[k], g = a.w_init[4 + k];
+    A[k] = w.x + g.x;
+    B[k] = g.y - w.y;
+    C[k] = w.y + g.y;
+    D[k] = w.x - g.x;
+  }
+  const float mu2 = 2.0f * a.mu;
+  const float MAG = 8388608.0f;
+  const float lcx = a.lcx - 0.5f + MAG, lcy = a.lcy - 0.5f + MAG;
+  const float glo = MAG, ghi = MAG + (float)(LMS_LUT_G - 1);
+  unsigned gated = 0;
+  float esum = 0.f;
+  int64_t pidx = 0;
+  if (MODE == 1) {
+    pidx = (a.n_off0 + n0) % a.P;
+    if (pidx < 0) pidx += a.P;
+  }
+  auto filt = [&](float2 u0, float2 u1, float2 u2, float2 u3) {
+    const float2 uu[4] = {u0, u1, u2, u3};
+    float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; k += 2) {
+      x0 = fmaf(A[k], uu[k].x, fmaf(B[k], uu[k].y, x0));
+      x1 = fmaf(A[k + 1], uu[k + 1].x, fmaf(B[k + 1], uu[k + 1].y, x1));
+      y0 = fmaf(C[k], uu[k].x, fmaf(D[k], uu[k].y, y0));
+      y1 = fmaf(C[k + 1], uu[k + 1].x, fmaf(D[k + 1], uu[k + 1].y, y1));
+    }
+    return make_float2(x0 + x1, y0 + y1);
+  };
+  auto dot2 = [](float2 u, float2 v) { return fmaf(u.x, v.x, u.y * v.y); };
+  // ring: R[i & 15] = W[i]; step j reads W[2j .. 2j+7] and refills W[2j+16], W[2j+17]
+  float2 R[16];
+  {
+    const float4* q = reinterpret_cast<const float4*>(xw);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 t = __ldcg(q + i);
+      R[2 * i] = make_float2(t.x, t.y);
+      R[2 * i + 1] = make_float2(t.z, t.w);
+    }
+  }
+  float qa = dot2(R[3], R[5]), qb = dot2(R[2], R[4]);
+  float2 y = filt(R[5], R[4], R[3], R[2]), ep = make_float2(0.f, 0.f);
+  auto step = [&](auto qc, int j) {
+    constexpr int q = decltype(qc)::value;  // j & 7
+    (void)MODE;
+    const float2 u0 = R[(2 * q + 5) & 15], u1 = R[(2 * q + 4) & 15], u2 = R[(2 * q + 3) & 15],
+                 u3 = R[(2 * q + 2) & 15];
+    const float2 v0 = R[(2 * q + 7) & 15], v1 = R[(2 * q + 6) & 15], w2 = R[(2 * q + 1) & 15], w3 = R[(2 * q) & 15];
+    const float4 nx = __ldcg(reinterpret_cast<const float4*>(xw + 2 * j + 16));
+    float2 ent = make_float2(0.f, 0.f);
+    bool out = false;
+    int pk = 0;
+    if (MODE == 1) {
+      pk = a.pattern[pidx];
+      pidx = (pidx + 1 == a.P) ? 0 : pidx + 1;
+    } else {
+      const float fx = fmaf(y.x, a.linv, lcx), fy = fmaf(y.y, a.linv, lcy);
+      const uint32_t cell = ((__float_as_uint(fy) << 10) | (__float_as_uint(fx) << 3)) & ((LMS_LUT_G * LMS_LUT_G - 1) << 3);
+      ent = *reinterpret_cast<const float2*>(reinterpret_cast<const unsigned char*>(s_lut) + cell);
+      out = (fx < glo) | (fx > ghi) | (fy < glo) | (fy > ghi) | (fx != fx) | (fy != fy);
+    }
+    {
+      const float2 pp[4] = {u2, u3, w2, w3};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        A[k] = fmaf(ep.x, pp[k].x, A[k]);
+        B[k] = fmaf(ep.x, pp[k].y, B[k]);
+        C[k] = fmaf(ep.y, pp[k].x, C[k]);
+        D[k] = fmaf(ep.y, pp[k].y, D[k]);
+      }
+    }
+    const float2 yh = filt(v0, v1, u0, u1);
+    const float q5 = dot2(u0, v0), q4 = dot2(u1, v1);
+    const float r = mu2 * (((q5 + q4) + qa) + qb);
+    float2 e, yn;
+    if (MODE == 1) {
+      const float2 ref = s_pts[pk];
+      e = make_float2(ref.x - y.x, ref.y - y.y);
+      yn = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
+    } else {
+      e = make_float2(ent.x - y.x, ent.y - y.y);
+      yn = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
+      if (out | isnan(yn.x)) {
+        const uint32_t w = out ? LMS_BRUTE : __float_as_uint(ent.y);
+        float d1 = INF, d2 = INF;
+        int k1 = 0;
+        if (w == LMS_BRUTE) {
+          for (int k = 0; k < a.m; ++k) {
+            const float dx = y.x - s_pts[k].x, dy = y.y - s_pts[k].y;
+            const float d = fmaf(dx, dx, dy * dy);
+            const bool bt = d < d1;
+            d2 = bt ? d1 : fminf(d2, d);
+            k1 = bt ? k : k1;
+            d1 = bt ? d : d1;
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int k = (int)((w >> (8 * jj)) & 0xffu);
+            const float dx = y.x - s_pts[k].x, dy = y.y - s_pts[k].y;
+            const float d = fmaf(dx, dx, dy * dy);
+            const bool bt = d < d1;
+            d2 = bt ? d1 : fminf(d2, d);
+            k1 = bt ? k : k1;
+            d1 = bt ? d : d1;
+          }
+        }
+        const float2 ref = s_pts[k1];
+        float gamma = 1.0f;
+        if (MODE == 0) gamma = fminf(1.0f, fmaxf(d2 - d1, 0.f) * a.inv_tau);
+        gated += (gamma < 1.0f) ? 1u : 0u;
+        e = make_float2(gamma * (ref.x - y.x), gamma * (ref.y - y.y));
+        yn = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
+      }
+    }
+    esum = fmaf(e.x, e.x, fmaf(e.y, e.y, esum));
+    y = yn;
+    ep = make_float2(mu2 * e.x, mu2 * e.y);
+    qa = q5;
+    qb = q4;
+    R[(2 * q) & 15] = make_float2(nx.x, nx.y);
+    R[(2 * q + 1) & 15] = make_float2(nx.z, nx.w);
+  };
+  const int K8 = a.K & ~7;
+#pragma unroll 1
+  for (int j = 0; j < K8; j += 8) {
+    step(Phase<0>{}, j);
+    step(Phase<1>{}, j + 1);
+    step(Phase<2>{}, j + 2);
+    step(Phase<3>{}, j + 3);
+    step(Phase<4>{}, j + 4);
+    step(Phase<5>{}, j + 5);
+    step(Phase<6>{}, j + 6);
+    step(Phase<7>{}, j + 7);
+  }
+  const int rem = a.K - K8;
+  if (rem > 0) step(Phase<0>{}, K8);
+  if (rem > 1) step(Phase<1>{}, K8 + 1);
+  if (rem > 2) step(Phase<2>{}, K8 + 2);
+  if (rem > 3) step(Phase<3>{}, K8 + 3);
+  if (rem > 4) step(Phase<4>{}, K8 + 4);
+  if (rem > 5) step(Phase<5>{}, K8 + 5);
+  if (rem > 6) step(Phase<6>{}, K8 + 6);
+  // the update of the last step: u_{K-1} = (W[2K+3], W[2K+2], W[2K+1], W[2K])
+  {
+    const float2 lastu[4] = {__ldcg(xw + 2 * a.K + 3), __ldcg(xw + 2 * a.K + 2), __ldcg(xw + 2 * a.K + 1),
+                             __ldcg(xw + 2 * a.K)};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      A[k] = fmaf(ep.x, lastu[k].x, A[k]);
+      B[k] = fmaf(ep.x, lastu[k].y, B[k]);
+      C[k] = fmaf(ep.y, lastu[k].x, C[k]);
+      D[k] = fmaf(ep.y, lastu[k].y, D[k]);
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a.taps[(int64_t)c * 8 + k] = make_float2(0.5f * (A[k] + D[k]), 0.5f * (C[k] - B[k]));
+      a.taps[(int64_t)c * 8 + 4 + k] = make_float2(0.5f * (A[k] - D[k]), 0.5f * (C[k] + B[k]));
+    }
+    if (gated) atomicAdd(&a.counts[b * 8 + C_GATED], (unsigned long long)gated);
+    bool bad = !(esum / (float)a.K <= 1.0f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) bad |= !isfinite(A[k] + B[k] + C[k] + D[k]);
+    if (bad) atomicOr(&a.counts[b * 8 + C_FLAGS], 1ull);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(LMSL_MAXW * 32) kk_lms_lanes_kernel(LmsArgs a) {
+  extern __shared__ __align__(128) unsigned char lmsl_smem[];
+  lms_lanes_body(a, lmsl_smem, blockIdx.x, MODE);
+}
+
 // ---------------------------------------------------------------------------
 // Kernel 1: the fused chain.  A persistent grid; each CTA walks a contiguous
 // range of the step list (segments of owners x steps).  Per 3072-sample step:
@@ -225,6 +457,12 @@ __device__ __forceinline__ StepPos decode_step(const ChainArgs& a, int64_t g) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(ChainArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  if (a.lms_ctas > 0 && (int)blockIdx.x >= (int)gridDim.x - a.lms_ctas) {
+    // the next batch's LMS update pass: these CTAs come last in the launch order and wait
+    // only for tail steps of this launch, which the chain CTAs never wait for
+    lms_lanes_body(a.lms, smem_raw, (int)blockIdx.x - ((int)gridDim.x - a.lms_ctas), a.lms_mode);
+    return;
+  }
   float2* s_tw = reinterpret_cast<float2*>(smem_raw);
   float2* s_H = reinterpret_cast<float2*>(smem_raw + SMEM_TW);
   float2* s_tw512 = reinterpret_cast<float2*>(smem_raw + SMEM_TW + SMEM_H);
@@ -269,7 +507,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
   const int warp = ((tid >> 5) + gi) & (NWARPS - 1), lane = tid & 31;
   const float invd = 1.0f / a.dc;
   const uint32_t n32 = (uint32_t)a.N;
-  const int64_t ngroups = (int64_t)gridDim.x * NGROUP, grp = (int64_t)blockIdx.x * NGROUP + gi;
+  const int64_t ngroups = (int64_t)(gridDim.x - a.lms_ctas) * NGROUP, grp = (int64_t)blockIdx.x * NGROUP + gi;
   const int64_t T = a.total_steps;
   const bool dyn = a.work_ctr != nullptr;
   int64_t g0 = dyn ? 0 : grp * T / ngroups;
@@ -673,15 +911,10 @@ cudaError_t launch_chain(const ChainArgs& a, int grid, cudaStream_t s) {
 //    index on ties), from which k1, D1 and D2 (second-smallest distance) follow
 //    exactly as in the oracle; cells with longer lists fall back to brute force.
 // ---------------------------------------------------------------------------
-constexpr size_t LMS_LUT_BYTES = (size_t)LMS_LUT_G * LMS_LUT_G * sizeof(float2);
 constexpr int LMS_CHUNK = 5632;  // update steps per shared-memory window of x2
 constexpr size_t LMS_SMEM_MAX = 220 * 1024;  // + static smem <= 227 KB
 static_assert(LMS_LUT_BYTES + (2 * LMS_CHUNK + 16) * sizeof(float2) <= LMS_SMEM_MAX, "LMS smem budget");
 
-template <int Q>
-struct Phase {
-  static constexpr int value = Q;
-};
 
 // one warp per chain; shared memory = [LUT (not in PILOT mode)] [x2 window of <= LMS_CHUNK steps]
 template <int MODE>  // 0: DD soft gate, 1: PILOT (known pattern), 2: DD hard (gamma = 1)
@@ -948,229 +1181,15 @@ cudaError_t launch_lms(const LmsArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------
-// Kernel 2b: LMS update pass with one LANE per chain (up to 512 chains per CTA,
-// all sharing one copy of the LMS table).  Same arithmetic and step order as
-// kk_lms_kernel; a warp's instruction stream serves 32 chains, so the whole
-// update pass of a batch occupies a single SM and runs concurrently with the
-// fused chain kernel of the previous batch (kk_rx_submit_batch pipeline).  The
-// x2 samples stream from L2 through a 16-register ring per lane, prefetched five
-// steps ahead.  Optionally spins until the chain kernel has published the x2
-// tails it reads (wait_ctr).
-// ---------------------------------------------------------------------------
-constexpr int LMSL_MAXW = 16;
-
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int MODE>  // 0: DD soft gate, 1: PILOT (known pattern), 2: DD hard (gamma = 1)
-__global__ void __launch_bounds__(LMSL_MAXW * 32) kk_lms_lanes_kernel(LmsArgs a) {
-  extern __shared__ __align__(128) unsigned char lmsl_smem[];
-  __shared__ float2 s_pts[129];
-  const float2* s_lut = reinterpret_cast<const float2*>(lmsl_smem);
-  const float INF = __int_as_float(0x7f800000);
-  if (MODE != 1) {
-    const float4* src = reinterpret_cast<const float4*>(a.lut);
-    float4* dst = reinterpret_cast<float4*>(lmsl_smem);
-    for (int i = threadIdx.x; i < LMS_LUT_G * LMS_LUT_G / 2; i += blockDim.x) dst[i] = __ldg(src + i);
-  }
-  for (int i = threadIdx.x; i < 129; i += blockDim.x) s_pts[i] = (i < a.m) ? a.pts[i] : make_float2(INF, INF);
-  __syncthreads();
-  if (a.wait_ctr) {
-    if ((threadIdx.x & 31) == 0)
-      while (ld_acquire_u64(a.wait_ctr) < a.wait_target) __nanosleep(200);
-    __syncwarp();
-  }
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = c < a.nchains;
-  const int cc = valid ? c : a.nchains - 1;  // idle lanes replay the last chain, results dropped
-  const int b = cc / a.nsub, sblk = cc - b * a.nsub;
-  const int64_t n0l = (int64_t)sblk * a.L - a.K;
-  const int64_t n0 = (int64_t)b * a.n_sym + n0l;
-  const float2* xw = a.x2_b0 + (int64_t)b * a.x2_stride + 2 * n0l - 4;  // W[i] = xw[i] (= x2[2 n0l - 4 + i])
-  float A[4], B[4], C[4], D[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float2 w = a.w_init[k], g = a.w_init[4 + k];
-    A[k] = w.x + g.x;
-    B[k] = g.y - w.y;
-    C[k] = w.y + g.y;
-    D[k] = w.x - g.x;
-  }
-  const float mu2 = 2.0f * a.mu;
-  const float MAG = 8388608.0f;
-  const float lcx = a.lcx - 0.5f + MAG, lcy = a.lcy - 0.5f + MAG;
-  const float glo = MAG, ghi = MAG + (float)(LMS_LUT_G - 1);
-  unsigned gated = 0;
-  float esum = 0.f;
-  int64_t pidx = 0;
-  if (MODE == 1) {
-    pidx = (a.n_off0 + n0) % a.P;
-    if (pidx < 0) pidx += a.P;
-  }
-  auto filt = [&](float2 u0, float2 u1, float2 u2, float2 u3) {
-    const float2 uu[4] = {u0, u1, u2, u3};
-    float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
-#pragma unroll
-    for (int k = 0; k < 4; k += 2) {
-      x0 = fmaf(A[k], uu[k].x, fmaf(B[k], uu[k].y, x0));
-      x1 = fmaf(A[k + 1], uu[k + 1].x, fmaf(B[k + 1], uu[k + 1].y, x1));
-      y0 = fmaf(C[k], uu[k].x, fmaf(D[k], uu[k].y, y0));
-      y1 = fmaf(C[k + 1], uu[k + 1].x, fmaf(D[k + 1], uu[k + 1].y, y1));
-    }
-    return make_float2(x0 + x1, y0 + y1);
-  };
-  auto dot2 = [](float2 u, float2 v) { return fmaf(u.x, v.x, u.y * v.y); };
-  // ring: R[i & 15] = W[i]; step j reads W[2j .. 2j+7] and refills W[2j+16], W[2j+17]
-  float2 R[16];
-  {
-    const float4* q = reinterpret_cast<const float4*>(xw);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float4 t = __ldcg(q + i);
-      R[2 * i] = make_float2(t.x, t.y);
-      R[2 * i + 1] = make_float2(t.z, t.w);
-    }
-  }
-  float qa = dot2(R[3], R[5]), qb = dot2(R[2], R[4]);
-  float2 y = filt(R[5], R[4], R[3], R[2]), ep = make_float2(0.f, 0.f);
-  auto step = [&](auto qc, int j) {
-    constexpr int q = decltype(qc)::value;  // j & 7
-    const float2 u0 = R[(2 * q + 5) & 15], u1 = R[(2 * q + 4) & 15], u2 = R[(2 * q + 3) & 15],
-                 u3 = R[(2 * q + 2) & 15];
-    const float2 v0 = R[(2 * q + 7) & 15], v1 = R[(2 * q + 6) & 15], w2 = R[(2 * q + 1) & 15], w3 = R[(2 * q) & 15];
-    const float4 nx = __ldcg(reinterpret_cast<const float4*>(xw + 2 * j + 16));
-    float2 ent = make_float2(0.f, 0.f);
-    bool out = false;
-    int pk = 0;
-    if (MODE == 1) {
-      pk = a.pattern[pidx];
-      pidx = (pidx + 1 == a.P) ? 0 : pidx + 1;
-    } else {
-      const float fx = fmaf(y.x, a.linv, lcx), fy = fmaf(y.y, a.linv, lcy);
-      const uint32_t cell = ((__float_as_uint(fy) << 10) | (__float_as_uint(fx) << 3)) & ((LMS_LUT_G * LMS_LUT_G - 1) << 3);
-      ent = *reinterpret_cast<const float2*>(reinterpret_cast<const unsigned char*>(s_lut) + cell);
-      out = (fx < glo) | (fx > ghi) | (fy < glo) | (fy > ghi) | (fx != fx) | (fy != fy);
-    }
-    {
-      const float2 pp[4] = {u2, u3, w2, w3};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        A[k] = fmaf(ep.x, pp[k].x, A[k]);
-        B[k] = fmaf(ep.x, pp[k].y, B[k]);
-        C[k] = fmaf(ep.y, pp[k].x, C[k]);
-        D[k] = fmaf(ep.y, pp[k].y, D[k]);
-      }
-    }
-    const float2 yh = filt(v0, v1, u0, u1);
-    const float q5 = dot2(u0, v0), q4 = dot2(u1, v1);
-    const float r = mu2 * (((q5 + q4) + qa) + qb);
-    float2 e, yn;
-    if (MODE == 1) {
-      const float2 ref = s_pts[pk];
-      e = make_float2(ref.x - y.x, ref.y - y.y);
-      yn = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
-    } else {
-      e = make_float2(ent.x - y.x, ent.y - y.y);
-      yn = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
-      if (out | isnan(yn.x)) {
-        const uint32_t w = out ? LMS_BRUTE : __float_as_uint(ent.y);
-        float d1 = INF, d2 = INF;
-        int k1 = 0;
-        if (w == LMS_BRUTE) {
-          for (int k = 0; k < a.m; ++k) {
-            const float dx = y.x - s_pts[k].x, dy = y.y - s_pts[k].y;
-            const float d = fmaf(dx, dx, dy * dy);
-            const bool bt = d < d1;
-            d2 = bt ? d1 : fminf(d2, d);
-            k1 = bt ? k : k1;
-            d1 = bt ? d : d1;
-          }
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int k = (int)((w >> (8 * jj)) & 0xffu);
-            const float dx = y.x - s_pts[k].x, dy = y.y - s_pts[k].y;
-            const float d = fmaf(dx, dx, dy * dy);
-            const bool bt = d < d1;
-            d2 = bt ? d1 : fminf(d2, d);
-            k1 = bt ? k : k1;
-            d1 = bt ? d : d1;
-          }
-        }
-        const float2 ref = s_pts[k1];
-        float gamma = 1.0f;
-        if (MODE == 0) gamma = fminf(1.0f, fmaxf(d2 - d1, 0.f) * a.inv_tau);
-        gated += (gamma < 1.0f) ? 1u : 0u;
-        e = make_float2(gamma * (ref.x - y.x), gamma * (ref.y - y.y));
-        yn = make_float2(fmaf(r, e.x, yh.x), fmaf(r, e.y, yh.y));
-      }
-    }
-    esum = fmaf(e.x, e.x, fmaf(e.y, e.y, esum));
-    y = yn;
-    ep = make_float2(mu2 * e.x, mu2 * e.y);
-    qa = q5;
-    qb = q4;
-    R[(2 * q) & 15] = make_float2(nx.x, nx.y);
-    R[(2 * q + 1) & 15] = make_float2(nx.z, nx.w);
-  };
-  const int K8 = a.K & ~7;
-#pragma unroll 1
-  for (int j = 0; j < K8; j += 8) {
-    step(Phase<0>{}, j);
-    step(Phase<1>{}, j + 1);
-    step(Phase<2>{}, j + 2);
-    step(Phase<3>{}, j + 3);
-    step(Phase<4>{}, j + 4);
-    step(Phase<5>{}, j + 5);
-    step(Phase<6>{}, j + 6);
-    step(Phase<7>{}, j + 7);
-  }
-  const int rem = a.K - K8;
-  if (rem > 0) step(Phase<0>{}, K8);
-  if (rem > 1) step(Phase<1>{}, K8 + 1);
-  if (rem > 2) step(Phase<2>{}, K8 + 2);
-  if (rem > 3) step(Phase<3>{}, K8 + 3);
-  if (rem > 4) step(Phase<4>{}, K8 + 4);
-  if (rem > 5) step(Phase<5>{}, K8 + 5);
-  if (rem > 6) step(Phase<6>{}, K8 + 6);
-  // the update of the last step: u_{K-1} = (W[2K+3], W[2K+2], W[2K+1], W[2K])
-  {
-    const float2 lastu[4] = {__ldcg(xw + 2 * a.K + 3), __ldcg(xw + 2 * a.K + 2), __ldcg(xw + 2 * a.K + 1),
-                             __ldcg(xw + 2 * a.K)};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      A[k] = fmaf(ep.x, lastu[k].x, A[k]);
-      B[k] = fmaf(ep.x, lastu[k].y, B[k]);
-      C[k] = fmaf(ep.y, lastu[k].x, C[k]);
-      D[k] = fmaf(ep.y, lastu[k].y, D[k]);
-    }
-  }
-  if (valid) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      a.taps[(int64_t)c * 8 + k] = make_float2(0.5f * (A[k] + D[k]), 0.5f * (C[k] - B[k]));
-      a.taps[(int64_t)c * 8 + 4 + k] = make_float2(0.5f * (A[k] - D[k]), 0.5f * (C[k] + B[k]));
-    }
-    if (gated) atomicAdd(&a.counts[b * 8 + C_GATED], (unsigned long long)gated);
-    bool bad = !(esum / (float)a.K <= 1.0f);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) bad |= !isfinite(A[k] + B[k] + C[k] + D[k]);
-    if (bad) atomicOr(&a.counts[b * 8 + C_FLAGS], 1ull);
-  }
-}
-
 int lms_lanes_ctas(int nchains) { return (nchains + LMSL_MAXW * 32 - 1) / (LMSL_MAXW * 32); }
 
 cudaError_t launch_lms_lanes(const LmsArgs& a, cudaStream_t s) {
   if (a.nchains < 1) return cudaSuccess;
   static bool attr_done = false;
   if (!attr_done) {
-    for (cudaError_t e : {cudaFuncSetAttribute(kk_lms_lanes_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LMS_LUT_BYTES),
-                          cudaFuncSetAttribute(kk_lms_lanes_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LMS_LUT_BYTES)})
+    for (cudaError_t e : {cudaFuncSetAttribute(kk_lms_lanes_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(LMS_LUT_BYTES + 129 * sizeof(float2))),
+                          cudaFuncSetAttribute(kk_lms_lanes_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(LMS_LUT_BYTES + 129 * sizeof(float2))),
+                          cudaFuncSetAttribute(kk_lms_lanes_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(LMS_LUT_BYTES + 129 * sizeof(float2)))})
       if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -1178,12 +1197,13 @@ cudaError_t launch_lms_lanes(const LmsArgs& a, cudaStream_t s) {
   const int per = (a.nchains + ctas - 1) / ctas;
   const int threads = ((per + 31) / 32) * 32;
   const int mode = (a.mode == 1) ? 1 : (a.mode == 2 || !(a.inv_tau > 0.f)) ? 2 : 0;
+  const size_t sm = LMS_LUT_BYTES + 129 * sizeof(float2);
   if (mode == 1)
-    kk_lms_lanes_kernel<1><<<ctas, threads, 0, s>>>(a);
+    kk_lms_lanes_kernel<1><<<ctas, threads, sm, s>>>(a);
   else if (mode == 2)
-    kk_lms_lanes_kernel<2><<<ctas, threads, LMS_LUT_BYTES, s>>>(a);
+    kk_lms_lanes_kernel<2><<<ctas, threads, sm, s>>>(a);
   else
-    kk_lms_lanes_kernel<0><<<ctas, threads, LMS_LUT_BYTES, s>>>(a);
+    kk_lms_lanes_kernel<0><<<ctas, threads, sm, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -1025,9 +1025,8 @@ static void slot_harvest(kk_rx_t* h, AsyncSlot& a) {
 
 // the fused chain of slot p (APPLY), optionally preceded in the same launch by the
 // x2 tails of slot t's batch (a leading SEG_X2_TAIL segment, published via the counter)
-static kk_status issue_chain(kk_rx_t* h, int p, int t) {
+static kk_status issue_chain(kk_rx_t* h, int p, int t, const LmsArgs* la) {
   AsyncSlot& ap = h->aslot[p];
-  CK(cudaStreamWaitEvent(h->stream, ap.ev_lms, 0));
   ChainArgs ca{};
   fill_chain_common(h, ca, ap.codes);
   const int S = h->steps_per_buf;
@@ -1039,7 +1038,11 @@ static kk_status issue_chain(kk_rx_t* h, int p, int t) {
                        nullptr, 0, at.codes};
     ca.tail_ctr = h->d_ctr;
     ca.aligned16 = ca.aligned16 && ((uintptr_t)at.codes % 16) == 0;
-    grid -= lms_lanes_ctas((int)at.nb);  // leave SMs to the concurrent LMS pass
+    if (la) {  // batch t's update pass rides along as the last CTAs of this launch
+      ca.lms = *la;
+      ca.lms_ctas = lms_lanes_ctas(la->nchains);
+      ca.lms_mode = (la->mode == 1) ? 1 : (la->mode == 2 || !(la->inv_tau > 0.f)) ? 2 : 0;
+    }
   }
   ca.seg[ns++] = Seg{0, (int32_t)ap.nb, 0, S, SEG_APPLY, 1, 0, 0, nullptr, ap.out_dev, ap.d_counts, ap.taps, ap.n_off0,
                      ap.codes};
@@ -1082,8 +1085,7 @@ extern "C" kk_status kk_rx_submit_batch(kk_rx_t* h, const int16_t* first, int64_
     int d;
     ~Restore() { cudaSetDevice(d); }
   } restore{cur};
-  if (!h->lms_stream) {
-    CK(cudaStreamCreateWithFlags(&h->lms_stream, cudaStreamNonBlocking));
+  if (!h->h2d_stream) {
     CK(cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
   }
@@ -1110,20 +1112,20 @@ extern "C" kk_status kk_rx_submit_batch(kk_rx_t* h, const int16_t* first, int64_
   a.n_off0 = n_off0;
   a.out_dev = (out_symbols && out_dev) ? out_symbols : a.d_out;
   a.out_host = (out_symbols && !out_dev) ? out_symbols : nullptr;
-  CK(cudaEventRecord(h->ev_in, h->stream));  // the caller's prior work on its stream
-  CK(cudaStreamWaitEvent(h->lms_stream, h->ev_in, 0));
   if (in_dev) {
     a.codes = first;
   } else {
-    // host input: pinned (or pageable) -> slot staging on the copy stream
-    CK(cudaStreamWaitEvent(h->h2d_stream, h->ev_in, 0));
+    // host input: pinned (or pageable) -> slot staging on the copy stream.  No wait on the
+    // compute stream: the data is in host memory, and the slot's previous batch has finished
+    // (host wait above), so copies run back to back while earlier batches compute.  The
+    // chain launch that first reads the batch (its tails) waits for this copy.
     CK(cudaMemcpyAsync(a.d_stage, first - h->left, (size_t)(h->left + nbuf * h->N + h->right) * sizeof(int16_t),
                        cudaMemcpyHostToDevice, h->h2d_stream));
     CK(cudaEventRecord(a.ev_h2d, h->h2d_stream));
-    CK(cudaStreamWaitEvent(h->lms_stream, a.ev_h2d, 0));
+    CK(cudaStreamWaitEvent(h->stream, a.ev_h2d, 0));
     a.codes = a.d_stage + h->left;
   }
-  CK(cudaMemsetAsync(a.d_counts, 0, (size_t)nbuf * 8 * sizeof(unsigned long long), h->lms_stream));
+  CK(cudaMemsetAsync(a.d_counts, 0, (size_t)nbuf * 8 * sizeof(unsigned long long), h->stream));
   LmsArgs la{};
   la.lut = h->d_lmslut;
   la.lcx = h->lms_lcx;
@@ -1156,27 +1158,22 @@ extern "C" kk_status kk_rx_submit_batch(kk_rx_t* h, const int16_t* first, int64_
     ca.seg[0] = Seg{-1, (int32_t)nbuf, h->pre_first, h->steps_per_buf, SEG_X2_TAIL, 0, 0, 0, a.tails,
                     nullptr, nullptr, nullptr, 0, a.codes};
     ca.total_steps = seg_steps(ca.seg[0]);
-    CK(launch_chain(ca, h->grid_chain, h->lms_stream));
+    CK(launch_chain(ca, h->grid_chain, h->stream));
     // nothing else runs yet: the one-warp-per-chain kernel (lowest latency, many SMs)
-    if (h->timing) CK(cudaEventRecord(a.ev_t[0], h->lms_stream));
-    CK(launch_lms(la, h->lms_stream));
-    if (h->timing) CK(cudaEventRecord(a.ev_t[1], h->lms_stream));
+    if (h->timing) CK(cudaEventRecord(a.ev_t[0], h->stream));
+    CK(launch_lms(la, h->stream));
+    if (h->timing) CK(cudaEventRecord(a.ev_t[1], h->stream));
+    a.timed_lms = h->timing;
     h->a_launches += 2;
+    a.state = 1;
   } else {
-    // this batch's update pass waits for its tails, computed first by the chain launch of batch p
+    // this batch's tails are the first work items of the chain launch of batch p, and its
+    // update pass runs as that launch's last CTAs (waiting on the tail counter)
     h->tail_done_target += (unsigned long long)nbuf * (unsigned long long)h->pre_steps;
     la.wait_ctr = h->d_ctr;
     la.wait_target = h->tail_done_target;
-    if (h->timing) CK(cudaEventRecord(a.ev_t[0], h->lms_stream));
-    CK(launch_lms_lanes(la, h->lms_stream));
-    if (h->timing) CK(cudaEventRecord(a.ev_t[1], h->lms_stream));
-    a.timed_lms = h->timing;
-    h->a_launches += 1;
-  }
-  CK(cudaEventRecord(a.ev_lms, h->lms_stream));
-  a.state = 1;
-  if (p >= 0) {
-    st = issue_chain(h, p, s);
+    a.state = 1;
+    st = issue_chain(h, p, s, &la);
     if (st != KK_OK) return st;
   }
   h->a_deferred = s;
@@ -1196,12 +1193,11 @@ extern "C" kk_status kk_rx_sync(kk_rx_t* h, kk_rx_counts* out_per_buf, int64_t m
     ~Restore() { cudaSetDevice(d); }
   } restore{cur};
   if (h->a_deferred >= 0) {
-    kk_status st = issue_chain(h, h->a_deferred, -1);
+    kk_status st = issue_chain(h, h->a_deferred, -1, nullptr);
     if (st != KK_OK) return st;
     h->a_deferred = -1;
   }
   CK(cudaStreamSynchronize(h->stream));
-  if (h->lms_stream) CK(cudaStreamSynchronize(h->lms_stream));
   for (int k = 0; k < h->a_norder; ++k) slot_harvest(h, h->aslot[h->a_order[k]]);
   h->a_norder = 0;
   const int64_t n = (int64_t)h->a_counts.size();
