@@ -140,28 +140,41 @@ __device__ __forceinline__ void dft_brin(float2 (&v)[N]) {
 //   in : x[lane + 32 n2] at v[brev5(n2)]  (lane layout, registers bit-reversed)
 //   out: X[lane + 32 k2] at v[k2]          (lane layout, natural)
 //   X[k] = sum_n x[n] e^{-2 pi i n k / 1024}
-// scr: this warp's 32 x 33 float tile; tw: shared table tw[r*32 + l] = e^{-2 pi i r l / 1024}.
+// scr: this warp's 32 x 33 float tile (wide: 32 x 32 float2); tw: shared table tw[r*32 + l] = e^{-2 pi i r l / 1024}.
 // One copy of the 32-point DFT: the two passes are a loop.
 __device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __restrict__ scr,
-                                        const float2* __restrict__ tw) {
+                                        const float2* __restrict__ tw, bool wide) {
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
     dft_brin<32>(v);
     if (pass == 0) {
 #pragma unroll
       for (int r = 1; r < 32; ++r) v[r] = c_mul(v[r], tw[r * 32 + lane]);
+      if (wide) {
+        // 64-bit transpose through a 32 x 32 float2 tile (needs 1024 float2 of scratch),
+        // columns XOR-swizzled by the row: both directions run at the 2-wavefront minimum
+        float2* s2 = reinterpret_cast<float2*>(scr);
 #pragma unroll
-      for (int r = 0; r < 32; ++r) scr[r * 33 + lane] = v[r].x;
-      __syncwarp();
+        for (int r = 0; r < 32; ++r) s2[r * 32 + (lane ^ r)] = v[r];
+        __syncwarp();
 #pragma unroll
-      for (int n = 0; n < 32; ++n) v[brev(n, 5)].x = scr[lane * 33 + n];
-      __syncwarp();
+        for (int n = 0; n < 32; ++n) v[brev(n, 5)] = s2[lane * 32 + (n ^ lane)];
+        __syncwarp();
+      } else {
+        // two 32-bit transposes through a padded 32 x 33 float tile
 #pragma unroll
-      for (int r = 0; r < 32; ++r) scr[r * 33 + lane] = v[r].y;
-      __syncwarp();
+        for (int r = 0; r < 32; ++r) scr[r * 33 + lane] = v[r].x;
+        __syncwarp();
 #pragma unroll
-      for (int n = 0; n < 32; ++n) v[brev(n, 5)].y = scr[lane * 33 + n];
-      __syncwarp();
+        for (int n = 0; n < 32; ++n) v[brev(n, 5)].x = scr[lane * 33 + n];
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 32; ++r) scr[r * 33 + lane] = v[r].y;
+        __syncwarp();
+#pragma unroll
+        for (int n = 0; n < 32; ++n) v[brev(n, 5)].y = scr[lane * 33 + n];
+        __syncwarp();
+      }
     }
   }
 }

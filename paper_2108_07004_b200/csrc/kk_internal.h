@@ -95,6 +95,7 @@ struct ChainArgs {
   int64_t x2h;             // tail length (x2 samples) = 2K + 64
   float dc, vmin, a_hat, invN;
   uint32_t tb_mod, s32;    // tone_bin mod N, (tb*32) mod N
+  float2 rot[16];          // e^{2 pi i ((tb 32 r) mod N) / N}, r = 0..15 (EQ output downconversion)
   const float2* tw1024;    // [32*32] e^{-2 pi i r l / 1024}
   const float2* tw512;     // [16*32] e^{-2 pi i r l / 512}
   const float2* Hs;        // [1024] DFT of the tone-shifted h, / 1024 (reading R5 + downconversion)
@@ -117,6 +118,9 @@ struct ChainArgs {
   // blocks; lane-per-chain body, waits on tail_ctr for the tails this launch computes)
   int32_t lms_ctas, lms_mode;
   LmsArgs lms;
+  // diagnostics (KKRX_PHASE_TIMING): per-group clock64 sums [0] staging, [1] phase H,
+  // [2] phase E, [3] phase A + step tail, [4] steps, [5] H task busy (3 warps), [6] E task busy (4 warps)
+  unsigned long long* dbg;
 };
 
 struct ApplyArgs {

@@ -672,7 +672,8 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
         const int nfft = isH ? 2 : 1;
 #pragma unroll 1
         for (int f = 0; f < nfft; ++f) {
-          fft1024(v, lane, scr, s_tw);
+          // H tasks: 64-bit transposes through their own 1024-sample output slice
+          fft1024(v, lane, scr, s_tw, isH && !wt);
           if (isH && f == 0) {
             // S2: phi = -H{l} <-> +i sgn(k) L_k (reading R1; the /1024 is in S1), conjugated so the
             // next forward FFT computes the inverse: IFFT(Y) = conj(FFT(conj(Y)))
@@ -705,17 +706,24 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
             dst[lane + 32 * n2].y = v[n2].x;
             dst[lane + 32 * n2 + 512].y = -v[n2].y;
           }
-#pragma unroll 4
-          for (int t = 0; t < 32; ++t) {
-            const int mm = lane + 32 * (t & 15) + 256 + 512 * (t >> 4);
-            const float phi = dst[mm].y;
-            const int16_t code = src[s_off + mm];
-            const float vv = fmaxf((float)code + a.dc, a.vmin);
-            const float amp = vv * rsqrt_ftz(vv);
-            float sp, cp;
-            sincos_small(phi, &sp, &cp);  // |phi| of a few rad at most (KK phase)
-            dst[mm] = make_float2(fmaf(amp, cp, -a.a_hat), amp * sp);
-            clip += ((float)code + a.dc < a.vmin && mm < lim) ? 1u : 0u;
+          // outputs mm = lane + 256 + 32 t (chunk c0) and mm + 512 (chunk c0 + 1), t = 0..15
+          const int16_t* sp0 = src + s_off + lane + 256;
+          float2* dp0 = dst + lane + 256;
+          const bool allin = lim >= 1280;  // every output position of this task is < N
+#pragma unroll 2
+          for (int t = 0; t < 16; ++t) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int o = 32 * t + 512 * hh;
+              const float phi = dp0[o].y;
+              const float cv = (float)sp0[o] + a.dc;
+              const float vv = fmaxf(cv, a.vmin);
+              const float amp = vv * rsqrt_ftz(vv);
+              float sp, cp;
+              sincos_small(phi, &sp, &cp);  // |phi| of a few rad at most (KK phase)
+              dp0[o] = make_float2(fmaf(amp, cp, -a.a_hat), amp * sp);
+              clip += (cv < a.vmin && (allin || lane + 256 + o < lim)) ? 1u : 0u;
+            }
           }
           if (cnt) acc_clip += clip;
           if (wt) {
@@ -780,16 +788,18 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
             hi2 = (int)(h2 < hi2 ? (h2 > 0 ? h2 : 0) : hi2);
             dptr = sg.x2dst + dbase + (P0 >> 1);
           }
-          uint32_t qi = add_mod(q_step, q_lane, n32);  // (tb * P0) mod N
+          // e^{i theta_P} at P = P0 + 32 r2: one sincos for the lane's base, times the
+          // constant e^{i theta(32 r2)} (host fp64, rounded once; kernel-parameter operands)
+          float sb, cb;
+          cis_turns((float)add_mod(q_step, q_lane, n32) * a.invN, &sb, &cb);  // (tb * P0) mod N
 #pragma unroll
           for (int r2 = 0; r2 < 16; ++r2) {
             if (r2 >= lo2 && r2 < hi2) {
-              float st, ct;
-              cis_turns((float)qi * a.invN, &st, &ct);
+              const float2 rr = a.rot[r2];
+              const float ct = fmaf(cb, rr.x, -sb * rr.y), st = fmaf(cb, rr.y, sb * rr.x);
               const float2 o = z[r2];
               dptr[16 * r2] = make_float2(o.x * ct + o.y * st, o.x * st - o.y * ct);  // conj(o) e^{i theta}
             }
-            qi = add_mod(qi, a.s32, n32);
           }
         }
       }
@@ -825,6 +835,12 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
       }
       float2 yv[SPT];
       uint32_t cw[SPT];
+      float2 ta[4], tc[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ta[q] = s_taps[q];
+        tc[q] = s_taps[4 + q];
+      }
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
         // y = w^T u + g^T u* with u = (xs[2s+3], xs[2s+2], xs[2s+1], xs[2s]), factored taps
@@ -833,9 +849,8 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
         float2 y = make_float2(0.f, 0.f);
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          const float2 ta = s_taps[t], tc = s_taps[4 + t];
-          y.x = fmaf(ta.x, u[t].x, fmaf(ta.y, u[t].y, y.x));
-          y.y = fmaf(tc.x, u[t].x, fmaf(tc.y, u[t].y, y.y));
+          y.x = fmaf(ta[t].x, u[t].x, fmaf(ta[t].y, u[t].y, y.x));
+          y.y = fmaf(tc[t].x, u[t].x, fmaf(tc[t].y, u[t].y, y.y));
         }
         yv[k] = y;
         cw[k] = lut_word(y, a.lut, s_lut, lut_smem);

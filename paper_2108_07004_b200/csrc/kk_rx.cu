@@ -672,6 +672,11 @@ static void fill_chain_common(kk_rx_t* h, ChainArgs& ca, const int16_t* codes_de
   ca.invN = (float)(1.0 / (double)h->N);
   ca.tb_mod = h->tb_mod;
   ca.s32 = h->s32;
+  for (int r = 0; r < 16; ++r) {
+    const int64_t ph = ((int64_t)h->tb_mod * 32 * r) % h->N;
+    const double t = -0.0 + 2.0 * M_PI * (double)ph / (double)h->N;
+    ca.rot[r] = make_float2((float)std::cos(t), (float)std::sin(t));
+  }
   ca.tw1024 = h->d_tw;
   ca.tw512 = h->d_tw512;
   ca.Hs = h->d_H;
