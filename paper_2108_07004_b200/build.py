@@ -27,6 +27,7 @@ def build(verbose=False, force=False, out=None, csrc=None, include=None):
     if not force and os.path.exists(OUT_) and all(os.path.getmtime(OUT_) >= os.path.getmtime(d) for d in deps):
         return OUT_
     flags = [f if f != os.path.join(os.path.dirname(HERE), "include") else INC_ for f in FLAGS]
+    flags += os.environ.get("KK_EXTRA_NVCC_FLAGS", "").split() if out is not None else []
     cmd = [NVCC, *ARCH, *flags, "-shared", "-o", OUT_ + ".tmp", *srcs, "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode != 0:

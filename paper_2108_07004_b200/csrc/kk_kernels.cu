@@ -18,6 +18,10 @@
 #include "kk_fft.cuh"
 #include "kk_internal.h"
 
+#ifndef KK_PHASE_TIMING
+#define KK_PHASE_TIMING 0
+#endif
+
 namespace kk {
 
 // compile-time phase tag of unrolled loop bodies
@@ -202,6 +206,15 @@ struct StepPos {
 };
 
 __device__ __forceinline__ int64_t seg_steps_dev(const Seg& s) { return (int64_t)s.n_own * (s.i_end - s.i_begin); }
+
+// the step after p in the step list (segments of owners x steps), without divisions
+__device__ __forceinline__ StepPos next_step(const ChainArgs& a, StepPos p) {
+  const Seg& sg = a.seg[p.s];
+  if (p.i + 1 < sg.i_end) return StepPos{p.s, p.o, p.i + 1};
+  if (p.o + 1 < sg.owner_first + sg.n_own) return StepPos{p.s, p.o + 1, (int64_t)sg.i_begin};
+  if (p.s + 1 < a.nseg) return StepPos{p.s + 1, a.seg[p.s + 1].owner_first, (int64_t)a.seg[p.s + 1].i_begin};
+  return StepPos{-1, 0, 0};
+}
 
 __device__ __forceinline__ StepPos decode_step(const ChainArgs& a, int64_t g) {
   StepPos r{0, 0, 0};
@@ -513,7 +526,18 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
   int64_t g0 = dyn ? 0 : grp * T / ngroups;
   int64_t g1 = dyn ? 0 : (grp + 1) * T / ngroups;
   __shared__ long long s_grab[NGROUP][2];
+  __shared__ long long s_pb[NGROUP];  // pattern index of this step's first symbol (thread 0 -> phase A)
   unsigned long long seen = 0;  // (tid 0) last observed work counter
+#if KK_PHASE_TIMING
+  long long tdbg[7] = {0, 0, 0, 0, 0, 0, 0};  // diagnostics (a.dbg; build with -DKK_PHASE_TIMING=1)
+  long long tmark = 0;
+#define KK_DBG(stmt) \
+  if (a.dbg) {       \
+    stmt;            \
+  }
+#else
+#define KK_DBG(stmt)
+#endif
   unsigned pphase = 0;
   int prev_s = -1, prev_o = -1000000;
   int64_t prev_i = -1000000;
@@ -574,7 +598,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     const Seg& sg = a.seg[s];
     const int mode = sg.mode;
     const bool warm = !(s == prev_s && owner == prev_o && i == prev_i + 1);
-    StepPos nxt = (g + 1 < g1) ? decode_step(a, g + 1) : StepPos{-1, 0, 0};
+    StepPos nxt = (g + 1 < g1) ? next_step(a, cur) : StepPos{-1, 0, 0};
     const bool next_cont = (g + 1 < g1) && nxt.s == s && nxt.o == owner && nxt.i == i + 1;
     if (s != prev_s || owner != prev_o) {
       flush(prev_s, prev_o);
@@ -592,6 +616,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     q_step = warm ? tone_index(a, sbase) : add_mod(q_step, s3072, n32);
     const int64_t wbase = (int64_t)STEP * i - 1280;  // owner position of wstg[0]
 
+    KK_DBG(tmark = clock64())
     // ---- codes of this step
     if (prefetched) {
       mbar_wait(bar, phase_bit);
@@ -614,10 +639,15 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     }
     // pattern bytes of this step's symbols (APPLY with counting): bulk copy, waited for in phase A
     const bool count_ref = (mode == SEG_APPLY) && a.pattern != nullptr;
+    if (count_ref && !a.pat_tma && tid == 0) {
+      int64_t pb = (sg.n_off + (int64_t)(owner - sg.owner_first) * a.n_sym + (int64_t)SYM_PER_STEP * i - 32) % a.P;
+      s_pb[gi] = pb < 0 ? pb + a.P : pb;
+    }
     if (count_ref && a.pat_tma) {
       if (tid == 0) {
         int64_t pb = (sg.n_off + (int64_t)(owner - sg.owner_first) * a.n_sym + (int64_t)SYM_PER_STEP * i - 32) % a.P;
         if (pb < 0) pb += a.P;
+        s_pb[gi] = pb;
         const int64_t pa = pb & ~(int64_t)15;
         const unsigned len = (unsigned)(((pb - pa) + SYM_PER_STEP + 15) & ~15);
         const unsigned len1 = (pa + len <= a.P) ? len : (unsigned)(a.P - pa);
@@ -630,10 +660,14 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     }
     group_sync(gi);
 
+    KK_DBG(const long long t = clock64(); tdbg[0] += t - tmark; tmark = t)
     // ---- phase 0: Hilbert pairs (warps 0-2, warp 3 = warm-up pair); phase 1: EQ blocks
 #pragma unroll 1
     for (int phase = 0; phase < 2; ++phase) {
       const bool isH = phase == 0;
+#if KK_PHASE_TIMING
+      const long long tph = a.dbg ? clock64() : 0;
+#endif
       if (!isH) {
         // stg is free now: prefetch the next step's codes (async proxy) behind phases E and A
         prefetched = next_cont && a.aligned16;
@@ -802,8 +836,10 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
             }
           }
         }
+        KK_DBG(tdbg[isH ? 5 : 6] += clock64() - tph)
       }
       group_sync(gi);
+      KK_DBG(const long long t = clock64(); tdbg[isH ? 1 : 2] += t - tmark; tmark = t)
     }
 
     if (mode == SEG_APPLY) {
@@ -817,14 +853,11 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
         if (a.pat_tma) {
           mbar_wait(pbar, pphase);
           pphase ^= 1u;
-          int64_t pb = (sg.n_off + ko * a.n_sym + nbase) % a.P;
-          if (pb < 0) pb += a.P;
-          const int off = (int)(pb & 15);
+          const int off = (int)(s_pb[gi] & 15);
 #pragma unroll
           for (int k = 0; k < SPT; ++k) refv[k] = spat[off + tid + NWARPS * 32 * k];
         } else {
-          int64_t pb = (sg.n_off + ko * a.n_sym + nbase) % a.P;
-          if (pb < 0) pb += a.P;
+          const int64_t pb = s_pb[gi];
 #pragma unroll
           for (int k = 0; k < SPT; ++k) {
             int64_t pi = pb + tid + NWARPS * 32 * k;
@@ -879,6 +912,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
       __threadfence();
       atomicAdd(a.tail_ctr, 1ull);
     }
+    KK_DBG(tdbg[3] += clock64() - tmark; tdbg[4] += 1)
     prev_s = s;
     prev_o = owner;
     prev_i = i;
@@ -887,6 +921,18 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
   if (!dyn) break;
   }
   flush(prev_s, prev_o);
+#if KK_PHASE_TIMING
+  if (a.dbg) {
+    // group totals from the group's thread 0 (wall-clock phases), busy times from every lane 0
+    if (tid == 0)
+      for (int k = 0; k < 5; ++k) atomicAdd(a.dbg + k, (unsigned long long)tdbg[k]);
+    if (lane == 0) {
+      atomicAdd(a.dbg + 5, (unsigned long long)tdbg[5]);
+      atomicAdd(a.dbg + 6, (unsigned long long)tdbg[6]);
+    }
+  }
+#endif
+#undef KK_DBG
 }
 
 cudaError_t chain_setup(int device, int* grid_out) {

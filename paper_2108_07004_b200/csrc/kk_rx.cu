@@ -79,6 +79,7 @@ struct kk_rx {
   int ctr_next = 0;
   unsigned long long tail_done_target = 0;
   bool dyn_sched = true;
+  unsigned long long* d_dbg = nullptr;     // KKRX_PHASE_TIMING diagnostics
   // asynchronous pipeline
   static constexpr int NSLOT = 3;         // batches in flight: LMS(j) | chain(j-1) queued | chain(j-2) running
   AsyncSlot aslot[NSLOT];
@@ -377,6 +378,16 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
   cudaGetDevice(&cur);
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->d_dbg) {
+    unsigned long long t[8] = {0};
+    cudaMemcpy(t, h->d_dbg, sizeof(t), cudaMemcpyDeviceToHost);
+    const double st = t[4] ? (double)t[4] : 1.0;
+    std::fprintf(stderr,
+                 "KKRX_PHASE_TIMING steps %llu  cycles/step: staging %.0f  H %.0f  E %.0f  A+tail %.0f  |  "
+                 "busy/task: H %.0f  E %.0f\n",
+                 t[4], t[0] / st, t[1] / st, t[2] / st, t[3] / st, t[5] / st / 3.0, t[6] / st / 4.0);
+    cudaFree(h->d_dbg);
+  }
   if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
   void* ptrs[] = {h->d_tw,     h->d_tw512,  h->d_H,      h->d_pts,    h->d_winit,    h->d_lut,
                   h->d_lab,    h->d_pattern, h->d_lmslut, h->d_ctr, h->d_tails, h->d_taps,   h->d_counts,   h->d_out,
@@ -634,6 +645,12 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   CKC(cudaMalloc(&h->d_ctr, 64 * sizeof(unsigned long long)));
   CKC(cudaMemset(h->d_ctr, 0, 64 * sizeof(unsigned long long)));
   if (const char* e = std::getenv("KKRX_STATIC_SCHED")) h->dyn_sched = (e[0] == '0');
+  if (const char* e = std::getenv("KKRX_PHASE_TIMING")) {
+    if (e[0] == '1') {
+      CKC(cudaMalloc(&h->d_dbg, 8 * sizeof(unsigned long long)));
+      CKC(cudaMemset(h->d_dbg, 0, 8 * sizeof(unsigned long long)));
+    }
+  }
   CKC(cudaGetLastError());
 #undef CKC
   *out = h;
@@ -665,6 +682,7 @@ static bool is_device_ptr(const void* p) {
 
 static void fill_chain_common(kk_rx_t* h, ChainArgs& ca, const int16_t* codes_dev) {
   ca.N = h->N;
+  ca.dbg = h->d_dbg;
   ca.x2h = h->x2h;
   ca.dc = h->dc;
   ca.vmin = h->vmin;
