@@ -138,8 +138,34 @@ __device__ __forceinline__ int decide_word(float2 y, uint32_t w, const float2* _
   return kb;
 }
 
+// branch-free cell of y (clamped into the grid; the outer ring of cells is brute force)
+__device__ __forceinline__ int lut_cell(float2 y, const DecLut& L) {
+  const float gm = (float)(L.g - 1);
+  const float fx = fminf(fmaxf((y.x - L.x0) * L.inv, 0.f), gm), fy = fminf(fmaxf((y.y - L.y0) * L.inv, 0.f), gm);
+  return (int)fy * L.g + (int)fx;
+}
+
+// argmin over the 4 ascending candidates of a table word: pairwise tournament, strict <
+// keeps the lower index on ties (pad entries repeat the first candidate)
+__device__ __forceinline__ int decide4(float2 y, uint32_t w, const float2* __restrict__ sp) {
+  int k[4];
+  float d[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    k[c] = (int)((w >> (7 * c)) & 127u);
+    const float2 p = sp[k[c]];
+    const float dx = y.x - p.x, dy = y.y - p.y;
+    d[c] = fmaf(dx, dx, dy * dy);
+  }
+  const bool b01 = d[1] < d[0], b23 = d[3] < d[2];
+  const float m01 = b01 ? d[1] : d[0], m23 = b23 ? d[3] : d[2];
+  const int k01 = b01 ? k[1] : k[0], k23 = b23 ? k[3] : k[2];
+  return (m23 < m01) ? k23 : k01;
+}
+
 __device__ __forceinline__ int decide(float2 y, const DecLut& L, const float2* __restrict__ sp, int m) {
-  return decide_word(y, lut_word(y, L, nullptr, false), sp, m);
+  const uint32_t w = (L.g > 0) ? __ldg(L.cell + lut_cell(y, L)) : LUT_BRUTE;
+  return (w & LUT_BRUTE) ? decide_brute(y, sp, m) : decide4(y, w, sp);
 }
 
 __device__ __forceinline__ float2 wl_out(const float2 (&w)[4], const float2 (&g)[4], float2 u0, float2 u1, float2 u2,
@@ -868,32 +894,58 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
       }
       float2 yv[SPT];
       uint32_t cw[SPT];
-      float2 ta[4], tc[4];
+      {
+        float2 ta[4], tc[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        ta[q] = s_taps[q];
-        tc[q] = s_taps[4 + q];
+        for (int q = 0; q < 4; ++q) {
+          ta[q] = s_taps[q];
+          tc[q] = s_taps[4 + q];
+        }
+        // stage 1: y = w^T u + g^T u* with u = (xs[2s+3], xs[2s+2], xs[2s+1], xs[2s]), factored taps
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+          const int sidx = tid + NWARPS * 32 * k;
+          const float2 u[4] = {xs[2 * sidx + 3], xs[2 * sidx + 2], xs[2 * sidx + 1], xs[2 * sidx]};
+          float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
+#pragma unroll
+          for (int t = 0; t < 4; t += 2) {
+            x0 = fmaf(ta[t].x, u[t].x, fmaf(ta[t].y, u[t].y, x0));
+            x1 = fmaf(ta[t + 1].x, u[t + 1].x, fmaf(ta[t + 1].y, u[t + 1].y, x1));
+            y0 = fmaf(tc[t].x, u[t].x, fmaf(tc[t].y, u[t].y, y0));
+            y1 = fmaf(tc[t + 1].x, u[t + 1].x, fmaf(tc[t + 1].y, u[t + 1].y, y1));
+          }
+          yv[k] = make_float2(x0 + x1, y0 + y1);
+        }
       }
+      // stage 2: table words (branch-free cell index; uniform table location)
+      if (lut_smem) {
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) cw[k] = s_lut[lut_cell(yv[k], a.lut)];
+      } else {
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) cw[k] = (a.lut.g > 0) ? __ldg(a.lut.cell + lut_cell(yv[k], a.lut)) : LUT_BRUTE;
+      }
+      // stage 3: decisions from the candidate lists; brute force (off-grid / crowded
+      // cells, or no table) as a rare warp-uniform second pass
+      int dk[SPT];
+      bool anyb = false;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
-        // y = w^T u + g^T u* with u = (xs[2s+3], xs[2s+2], xs[2s+1], xs[2s]), factored taps
-        const int sidx = tid + NWARPS * 32 * k;
-        const float2 u[4] = {xs[2 * sidx + 3], xs[2 * sidx + 2], xs[2 * sidx + 1], xs[2 * sidx]};
-        float2 y = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          y.x = fmaf(ta[t].x, u[t].x, fmaf(ta[t].y, u[t].y, y.x));
-          y.y = fmaf(tc[t].x, u[t].x, fmaf(tc[t].y, u[t].y, y.y));
-        }
-        yv[k] = y;
-        cw[k] = lut_word(y, a.lut, s_lut, lut_smem);
+        dk[k] = decide4(yv[k], cw[k], s_pts);
+        anyb |= (cw[k] & LUT_BRUTE) != 0;
       }
+      if (__any_sync(0xffffffffu, anyb)) {
+#pragma unroll
+        for (int k = 0; k < SPT; ++k)
+          if (cw[k] & LUT_BRUTE) dk[k] = decide_brute(yv[k], s_pts, a.m);
+      }
+      // stage 4: labels out, error counts
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
         const int sidx = tid + NWARPS * 32 * k;
         const int n = nbase + sidx;
         if (n >= 0 && n < (int)a.n_sym) {
-          const int d = decide_word(yv[k], cw[k], s_pts, a.m);
+          const int d = dk[k];
           const uint8_t ld = s_lab[d];
           outp[n] = ld;
           if (count_ref) {

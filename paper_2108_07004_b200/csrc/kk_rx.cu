@@ -175,6 +175,12 @@ static bool build_lut_g(const std::vector<double>& pts, int m, int G, DecLut& L,
   std::vector<double> mind(m);
   for (int cy = 0; cy < G; ++cy)
     for (int cx = 0; cx < G; ++cx) {
+      if (cx == 0 || cy == 0 || cx == G - 1 || cy == G - 1) {
+        // outer ring: the kernel clamps y into the grid, so these cells also receive every
+        // y outside it -> brute force (not counted as crowded)
+        cells[(size_t)cy * G + cx] = 1u << 31;
+        continue;
+      }
       const double e = 1e-3 * cs;
       const double xl = x0 + cx * cs - e, xh = x0 + (cx + 1) * cs + e;
       const double yl = y0 + cy * cs - e, yh = y0 + (cy + 1) * cs + e;
