@@ -30,8 +30,10 @@ enum SegMode { SEG_APPLY = 0, SEG_X2_TAIL = 1, SEG_X2_FULL = 2 };
 // padded with their first index) | bit 31 = brute force (crowded cell)
 struct DecLut {
   const uint32_t* cell;            // [g*g]
-  float x0, y0, inv;               // cell (cx, cy) covers [x0 + cx/inv, ...)
-  int g;                           // grid size (0 = no LUT: always brute force)
+  float x0, y0, inv;               // cell (cx, cy) covers [x0 + cx/inv, ...); -x0*inv, -y0*inv are half-integers
+  int g;                           // grid size (0 = no LUT: always brute force), 64 or 128
+  float cxm, cym;                  // -x0*inv - 1/2 + 2^23 (exact): y*inv + cxm rounds to floor(cell) + 2^23
+  int lg;                          // log2(g)
 };
 
 // A segment of the step list: owners o = owner_first + k (k in [0, n_own)),

@@ -138,11 +138,13 @@ __device__ __forceinline__ int decide_word(float2 y, uint32_t w, const float2* _
   return kb;
 }
 
-// branch-free cell of y (clamped into the grid; the outer ring of cells is brute force)
+// branch-free cell of y (clamped into the grid; the outer ring of cells is brute force).
+// float->int by the 2^23 magic number folded into the FFMA (exact half-integer origin)
 __device__ __forceinline__ int lut_cell(float2 y, const DecLut& L) {
-  const float gm = (float)(L.g - 1);
-  const float fx = fminf(fmaxf((y.x - L.x0) * L.inv, 0.f), gm), fy = fminf(fmaxf((y.y - L.y0) * L.inv, 0.f), gm);
-  return (int)fy * L.g + (int)fx;
+  const float lo = 8388608.0f, hi = 8388608.0f + (float)(L.g - 1);
+  const float fx = fminf(fmaxf(fmaf(y.x, L.inv, L.cxm), lo), hi), fy = fminf(fmaxf(fmaf(y.y, L.inv, L.cym), lo), hi);
+  const int m = L.g - 1;
+  return ((int)(__float_as_uint(fy) & m) << L.lg) | (int)(__float_as_uint(fx) & m);
 }
 
 // argmin over the 4 ascending candidates of a table word: pairwise tournament, strict <

@@ -167,8 +167,11 @@ static bool build_lut_g(const std::vector<double>& pts, int m, int G, DecLut& L,
   }
   const double pad = 2.0 * dmin;
   const double span = std::max(xmax - xmin, ymax - ymin) + 2 * pad;
-  const float x0 = (float)(xmin - pad), y0 = (float)(ymin - pad);
   const float inv = (float)(G / span);
+  // origin snapped so that -x0*inv is a half-integer: the kernel's y*inv + (-x0*inv - 1/2 + 2^23)
+  // then rounds (single fp32 rounding) to 2^23 + floor((y - x0)*inv)
+  const double hx = std::floor(-(xmin - pad) * (double)inv) + 0.5, hy = std::floor(-(ymin - pad) * (double)inv) + 0.5;
+  const float x0 = (float)(-hx / (double)inv), y0 = (float)(-hy / (double)inv);
   const double cs = 1.0 / (double)inv;
   cells.assign((size_t)G * G, 0);
   int nb = 0;
@@ -214,6 +217,9 @@ static bool build_lut_g(const std::vector<double>& pts, int m, int G, DecLut& L,
   L.x0 = x0;
   L.y0 = y0;
   L.inv = inv;
+  L.cxm = (float)(hx - 0.5 + 8388608.0);
+  L.cym = (float)(hy - 0.5 + 8388608.0);
+  L.lg = (G == 128) ? 7 : 6;
   *n_brute = nb;
   return true;
 }
