@@ -667,15 +667,22 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     }
     // pattern bytes of this step's symbols (APPLY with counting): bulk copy, waited for in phase A
     const bool count_ref = (mode == SEG_APPLY) && a.pattern != nullptr;
-    if (count_ref && !a.pat_tma && tid == 0) {
-      int64_t pb = (sg.n_off + (int64_t)(owner - sg.owner_first) * a.n_sym + (int64_t)SYM_PER_STEP * i - 32) % a.P;
-      s_pb[gi] = pb < 0 ? pb + a.P : pb;
+    if (count_ref && tid == 0) {
+      // pattern index of symbol 768 i - 32: + 768 (mod P) along a run (the previous step's
+      // value is still in s_pb), one division otherwise; kept in smem, not in a register
+      int64_t pb_run;
+      if (!warm) {
+        pb_run = s_pb[gi] + SYM_PER_STEP;
+        while (pb_run >= a.P) pb_run -= a.P;
+      } else {
+        pb_run = (sg.n_off + (int64_t)(owner - sg.owner_first) * a.n_sym + (int64_t)SYM_PER_STEP * i - 32) % a.P;
+        if (pb_run < 0) pb_run += a.P;
+      }
+      s_pb[gi] = pb_run;
     }
     if (count_ref && a.pat_tma) {
       if (tid == 0) {
-        int64_t pb = (sg.n_off + (int64_t)(owner - sg.owner_first) * a.n_sym + (int64_t)SYM_PER_STEP * i - 32) % a.P;
-        if (pb < 0) pb += a.P;
-        s_pb[gi] = pb;
+        const int64_t pb = s_pb[gi];
         const int64_t pa = pb & ~(int64_t)15;
         const unsigned len = (unsigned)(((pb - pa) + SYM_PER_STEP + 15) & ~15);
         const unsigned len1 = (pa + len <= a.P) ? len : (unsigned)(a.P - pa);
