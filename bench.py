@@ -306,34 +306,47 @@ def run_gpu(args):
     # ---------------- e2e through the same C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
+        # the ADC's native packed 12-bit samples (1.5 B per sample) in pinned host memory, and
+        # the int16 form of the same codes (2 B per sample) for comparison
+        from synth.generate import pack12
+        h_packed = torch.from_numpy(pack12(stream_np)).pin_memory()
         h_stream = torch.from_numpy(stream_np).pin_memory()
         h_out = [torch.empty(B * (N // 4), dtype=torch.uint8).pin_memory() for _ in range(2)]
 
-        def submit_host(s):
+        def submit_host(s, packed):
             b0 = first_buf(s)
             rx.seek(b0)
-            rx.submit_batch(h_stream, off + b0 * N, B, h_out[s & 1])
+            if packed:
+                rx.submit_batch_packed12(h_packed, off + b0 * N, B, h_out[s & 1])
+            else:
+                rx.submit_batch(h_stream, off + b0 * N, B, h_out[s & 1])
 
-        submit_host(0)
-        rx.sync()
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(cur)
-        for s in range(args.steps):
-            submit_host(s)
-        rx.sync()
-        e1.record(cur)
-        torch.cuda.synchronize(dev)
-        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        h2d = (left + B * N + right) * 2
+        def e2e_run(packed):
+            submit_host(0, packed)
+            rx.sync()
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(cur)
+            for s in range(args.steps):
+                submit_host(s, packed)
+            rx.sync()
+            e1.record(cur)
+            torch.cuda.synchronize(dev)
+            et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            return samples_total / (float(et.item()) / 1e3) / 1e9
+
+        v_packed = e2e_run(True)
+        v_int16 = e2e_run(False)
+        span = left + B * N + right
         d2h = B * (N // 4) + B * 64
-        e2e = {"value": samples_total / (float(et.item()) / 1e3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        e2e = {"value": v_packed, "unit": UNIT, "h2d_bytes_per_step": span * 3 // 2, "d2h_bytes_per_step": d2h,
+               "input": "packed 12-bit ADC samples (kk_rx_submit_batch_packed12), pinned host memory",
+               "int16_input_value": v_int16, "int16_h2d_bytes_per_step": span * 2}
 
     if rank != 0:
         rx.close()

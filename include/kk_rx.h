@@ -154,6 +154,16 @@ kk_status kk_rx_process_batch(kk_rx_t *h, const int16_t *first, int64_t nbuf, ui
  * for bad arguments or nbuf > 4096. */
 kk_status kk_rx_submit_batch(kk_rx_t *h, const int16_t *first, int64_t nbuf, uint8_t *out_symbols);
 
+/* Same as kk_rx_submit_batch for the packed 12-bit ADC format: two two's-complement
+ * 12-bit codes per 3 bytes, little-endian (b0 = c0[7:0], b1 = c0[11:8] | c1[3:0] << 4,
+ * b2 = c1[11:4]); `first` points at the byte of the first buffer's first sample (its
+ * sample index must be even), the halos are readable in the same format.  Host or device
+ * memory; the handle copies 1.5 bytes per sample (host input: over PCIe on its copy stream)
+ * and unpacks on the GPU.  Results are bit-identical to the int16 path on the same codes.
+ * Errors as kk_rx_submit_batch; KK_EUNSUPPORTED if the halos or buffer_len are not
+ * multiples of 8 samples. */
+kk_status kk_rx_submit_batch_packed12(kk_rx_t *h, const uint8_t *first, int64_t nbuf, uint8_t *out_symbols);
+
 /* Finish every submitted batch and return their per-buffer counters in submission
  * order: up to max_out structs to out_per_buf (may be NULL), the total count to
  * *n_out (may be NULL).  Blocks until all outputs are valid. */

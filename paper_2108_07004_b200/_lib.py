@@ -71,6 +71,7 @@ EXPORTS = {
     "kk_rx_process_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(KKCounts)]),
     "kk_rx_seek": (C.c_int, [C.c_void_p, C.c_int64]),
     "kk_rx_submit_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "kk_rx_submit_batch_packed12": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "kk_rx_sync": (C.c_int, [C.c_void_p, C.POINTER(KKCounts), C.c_int64, C.POINTER(C.c_int64)]),
     "kk_rx_async_launches": (C.c_int64, [C.c_void_p]),
     "kk_rx_get_taps": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_float)]),

@@ -1330,6 +1330,44 @@ cudaError_t launch_lms_lanes(const LmsArgs& a, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
+// Kernel 4: packed 12-bit ADC samples -> int16 codes (S0 ingest of the packed input
+// format, kk_rx_submit_batch_packed12).  Two two's-complement 12-bit codes per 3 bytes,
+// little-endian: b0 = c0[7:0], b1 = c0[11:8] | c1[3:0] << 4, b2 = c1[11:4].  One thread
+// per 8 samples (12 bytes in, 16 bytes out); memory-bound (3.5 B per sample).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) kk_unpack12_kernel(const uint8_t* __restrict__ src, int16_t* __restrict__ dst,
+                                                          int64_t n8) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n8) return;
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(src + 12 * t);
+  const uint32_t w0 = __ldg(s), w1 = __ldg(s + 1), w2 = __ldg(s + 2);
+  // 96 bits = 8 codes of 12 bits, code k at bit 12 k
+  auto code = [&](int k) -> int16_t {
+    const int bit = 12 * k;
+    uint32_t v;
+    if (bit + 12 <= 32) v = w0 >> bit;
+    else if (bit < 32) v = (w0 >> bit) | (w1 << (32 - bit));
+    else if (bit + 12 <= 64) v = w1 >> (bit - 32);
+    else if (bit < 64) v = (w1 >> (bit - 32)) | (w2 << (64 - bit));
+    else v = w2 >> (bit - 64);
+    return (int16_t)((int32_t)(v << 20) >> 20);  // sign-extend 12 bits
+  };
+  uint4 o;
+  o.x = (uint16_t)code(0) | ((uint32_t)(uint16_t)code(1) << 16);
+  o.y = (uint16_t)code(2) | ((uint32_t)(uint16_t)code(3) << 16);
+  o.z = (uint16_t)code(4) | ((uint32_t)(uint16_t)code(5) << 16);
+  o.w = (uint16_t)code(6) | ((uint32_t)(uint16_t)code(7) << 16);
+  reinterpret_cast<uint4*>(dst)[t] = o;
+}
+
+cudaError_t launch_unpack12(const uint8_t* src, int16_t* dst, int64_t n_samples, cudaStream_t s) {
+  const int64_t n8 = n_samples / 8;
+  if (n8 <= 0) return cudaSuccess;
+  kk_unpack12_kernel<<<(unsigned)((n8 + 255) / 256), 256, 0, s>>>(src, dst, n8);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Kernel 3: fixed-tap WL apply, decision, demap, count from materialised x2
 // (used when sub_block < buffer: several tap sets per buffer)
 // ---------------------------------------------------------------------------

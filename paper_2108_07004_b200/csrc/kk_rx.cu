@@ -44,6 +44,8 @@ struct AsyncSlot {
   uint8_t* d_out = nullptr;                 // labels staging (host or NULL output) [cap * n_sym]
   int16_t* d_stage = nullptr;               // host input staging [left + cap*N + right]
   int64_t stage_cap = 0;
+  uint8_t* d_pack = nullptr;                // packed-12 input staging [1.5 (left + cap*N + right)]
+  int64_t pack_cap = 0;
   int64_t nb = 0, index = 0, n_off0 = 0;
   const int16_t* codes = nullptr;           // device samples of buffer 0 of the batch
   uint8_t* out_dev = nullptr;               // where the chain writes labels
@@ -410,7 +412,7 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
   if (h->lms_stream) cudaStreamSynchronize(h->lms_stream);
   if (h->h2d_stream) cudaStreamSynchronize(h->h2d_stream);
   for (AsyncSlot& a : h->aslot) {
-    void* ap[] = {a.tails, a.taps, a.d_counts, a.d_out, a.d_stage};
+    void* ap[] = {a.tails, a.taps, a.d_counts, a.d_out, a.d_stage, a.d_pack};
     for (void* q : ap)
       if (q) cudaFree(q);
     if (a.h_counts) cudaFreeHost(a.h_counts);
@@ -989,7 +991,7 @@ kk_status kk_rx_process_batch(kk_rx_t* h, const int16_t* first, int64_t nbuf, ui
 // kernel waits on their completion counter).  The chain of the newest batch is
 // deferred to the next submit or to kk_rx_sync.
 // ---------------------------------------------------------------------------
-static kk_status slot_reserve(kk_rx_t* h, AsyncSlot& a, int64_t nb, bool host_in) {
+static kk_status slot_reserve(kk_rx_t* h, AsyncSlot& a, int64_t nb, bool host_in, bool packed) {
   if (!a.ev_lms) {
     CK(cudaEventCreateWithFlags(&a.ev_lms, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&a.ev_done, cudaEventDisableTiming));
@@ -1014,12 +1016,19 @@ static kk_status slot_reserve(kk_rx_t* h, AsyncSlot& a, int64_t nb, bool host_in
     CK(cudaMallocHost(&a.h_counts, (size_t)nb * 8 * sizeof(unsigned long long)));
     a.cap = nb;
   }
-  if (host_in && nb > a.stage_cap) {
+  if ((host_in || packed) && nb > a.stage_cap) {
     if (a.d_stage) cudaFree(a.d_stage);
     a.d_stage = nullptr;
     a.stage_cap = 0;
     CK(cudaMalloc(&a.d_stage, (size_t)(h->left + nb * h->N + h->right) * sizeof(int16_t)));
     a.stage_cap = nb;
+  }
+  if (packed && nb > a.pack_cap) {
+    if (a.d_pack) cudaFree(a.d_pack);
+    a.d_pack = nullptr;
+    a.pack_cap = 0;
+    CK(cudaMalloc(&a.d_pack, (size_t)(h->left + nb * h->N + h->right) * 3 / 2 + 16));
+    a.pack_cap = nb;
   }
   return KK_OK;
 }
@@ -1106,7 +1115,12 @@ static kk_status issue_chain(kk_rx_t* h, int p, int t, const LmsArgs* la) {
   return KK_OK;
 }
 
-extern "C" kk_status kk_rx_submit_batch(kk_rx_t* h, const int16_t* first, int64_t nbuf, uint8_t* out_symbols) {
+// input formats of the submit path
+enum { IN_INT16 = 0, IN_PACKED12 = 1 };
+
+static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint8_t* out_symbols, int fmt) {
+  const int16_t* first = static_cast<const int16_t*>(first_v);
+  const uint8_t* first_b = static_cast<const uint8_t*>(first_v);
   if (!h) return fail(KK_EINVAL, "null handle");
   if (h->sticky != KK_OK) return fail(KK_ESTATE, "handle is in a failed state (previous CUDA error)");
   if (!first || nbuf <= 0) return fail(KK_EINVAL, "need a buffer pointer and nbuf > 0");
@@ -1124,8 +1138,10 @@ extern "C" kk_status kk_rx_submit_batch(kk_rx_t* h, const int16_t* first, int64_
     CK(cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
   }
-  const bool in_dev = is_device_ptr(first);
+  const bool in_dev = is_device_ptr(first_v);
   const bool out_dev = out_symbols ? is_device_ptr(out_symbols) : false;
+  const bool packed = fmt == IN_PACKED12;
+  if (packed && ((h->left | h->right | h->N) & 7)) return fail(KK_EUNSUPPORTED, "packed-12 input needs halos and N in multiples of 8");
   const int s = h->a_next;
   AsyncSlot& a = h->aslot[s];
   if (a.state == 2) {  // the chain of NSLOT submissions ago (normally finished): wait and harvest
@@ -1137,7 +1153,7 @@ extern "C" kk_status kk_rx_submit_batch(kk_rx_t* h, const int16_t* first, int64_
     }
   }
   if (a.state != 0) return fail(KK_ESTATE, "async slot busy");
-  kk_status st = slot_reserve(h, a, nbuf, !in_dev);
+  kk_status st = slot_reserve(h, a, nbuf, !in_dev, packed);
   if (st != KK_OK) return st;
   a.nb = nbuf;
   a.index = h->stream_index;
@@ -1147,7 +1163,19 @@ extern "C" kk_status kk_rx_submit_batch(kk_rx_t* h, const int16_t* first, int64_
   a.n_off0 = n_off0;
   a.out_dev = (out_symbols && out_dev) ? out_symbols : a.d_out;
   a.out_host = (out_symbols && !out_dev) ? out_symbols : nullptr;
-  if (in_dev) {
+  if (packed) {
+    // packed 12-bit samples (host or device) -> packed staging on the copy stream, unpacked
+    // there to int16 codes (1.5 instead of 2 bytes per sample cross PCIe)
+    const int64_t span = h->left + nbuf * h->N + h->right;
+    if (in_dev) CK(cudaEventRecord(h->ev_in, h->stream));  // device input: the caller's stream order
+    if (in_dev) CK(cudaStreamWaitEvent(h->h2d_stream, h->ev_in, 0));
+    CK(cudaMemcpyAsync(a.d_pack, first_b - h->left * 3 / 2, (size_t)(span * 3 / 2), cudaMemcpyDefault, h->h2d_stream));
+    CK(launch_unpack12(a.d_pack, a.d_stage, span, h->h2d_stream));
+    h->a_launches += 1;
+    CK(cudaEventRecord(a.ev_h2d, h->h2d_stream));
+    CK(cudaStreamWaitEvent(h->stream, a.ev_h2d, 0));
+    a.codes = a.d_stage + h->left;
+  } else if (in_dev) {
     a.codes = first;
   } else {
     // host input: pinned (or pageable) -> slot staging on the copy stream.  No wait on the
@@ -1215,6 +1243,15 @@ extern "C" kk_status kk_rx_submit_batch(kk_rx_t* h, const int16_t* first, int64_
   h->a_next = (s + 1) % kk_rx::NSLOT;
   h->stream_index += nbuf;
   return KK_OK;
+}
+
+extern "C" kk_status kk_rx_submit_batch(kk_rx_t* h, const int16_t* first, int64_t nbuf, uint8_t* out_symbols) {
+  return submit_impl(h, first, nbuf, out_symbols, IN_INT16);
+}
+
+extern "C" kk_status kk_rx_submit_batch_packed12(kk_rx_t* h, const uint8_t* first, int64_t nbuf,
+                                                 uint8_t* out_symbols) {
+  return submit_impl(h, first, nbuf, out_symbols, IN_PACKED12);
 }
 
 extern "C" kk_status kk_rx_sync(kk_rx_t* h, kk_rx_counts* out_per_buf, int64_t max_out, int64_t* n_out) {

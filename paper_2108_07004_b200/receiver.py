@@ -124,6 +124,19 @@ class KKReceiver:
         check(self._lib.kk_rx_submit_batch(self.h, C.c_void_p(base + 2 * int(offset)), int(nbuf),
                                            C.c_void_p(optr) if optr is not None else None), "kk_rx_submit_batch")
 
+    def submit_batch_packed12(self, packed, offset, nbuf, out=None):
+        """kk_rx_submit_batch_packed12: `packed` holds the stream in the packed 12-bit
+        format (uint8, 3 bytes per 2 samples; host or device); offset = sample index of
+        buffer 0's first sample (even)."""
+        base, es = _ptr(packed)
+        assert es == 1 and int(offset) % 2 == 0
+        optr = None
+        if out is not None:
+            optr, _ = _ptr(out)
+        check(self._lib.kk_rx_submit_batch_packed12(self.h, C.c_void_p(base + 3 * int(offset) // 2), int(nbuf),
+                                                    C.c_void_p(optr) if optr is not None else None),
+              "kk_rx_submit_batch_packed12")
+
     def sync(self, max_out=1 << 16):
         """kk_rx_sync: wait for every submitted batch; per-buffer counter dicts in order."""
         cnt = (KKCounts * int(max_out))()

@@ -266,6 +266,20 @@ def make_pool(cfg: LinkConfig, n_pool: int = 1, cache: bool = True, noiseless: b
     return pool
 
 
+def pack12(codes: np.ndarray) -> np.ndarray:
+    """int16 ADC codes (12-bit range) -> the packed 12-bit byte format of a 12-bit ADC:
+    two two's-complement codes per 3 bytes, little-endian (b0 = c0[7:0],
+    b1 = c0[11:8] | c1[3:0] << 4, b2 = c1[11:4]).  Input format only (no method arithmetic)."""
+    c = np.asarray(codes, dtype=np.int16)
+    assert c.size % 2 == 0
+    u = (c.astype(np.int32) & 0xFFF).reshape(-1, 2)
+    out = np.empty((u.shape[0], 3), dtype=np.uint8)
+    out[:, 0] = u[:, 0] & 0xFF
+    out[:, 1] = ((u[:, 0] >> 8) & 0x0F) | ((u[:, 1] & 0x0F) << 4)
+    out[:, 2] = (u[:, 1] >> 4) & 0xFF
+    return out.reshape(-1)
+
+
 def make_stream(pool: Pool, n_buffers: int, left: int, right: int, first: int = 0):
     """Contiguous int16 stream holding stream buffers first .. first+n_buffers-1
     plus `left` samples before and `right` after, cycling the pool in order.

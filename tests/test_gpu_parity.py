@@ -330,3 +330,35 @@ def test_async_full_size_bench_config():
     assert ro == rg
     a.close()
     b.close()
+
+
+def test_packed12_input_equals_int16():
+    """kk_rx_submit_batch_packed12 (host and device packed streams, unpacked on the GPU)
+    gives labels and counters bit-identical to the int16 submission of the same codes."""
+    _require_gpu()
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    from synth.generate import pack12
+    name = "C5_n16"
+    cfg = configs.get(name).link
+    pool = make_pool(cfg, 4)
+    fir = _fir(name)
+    left, right = halo_for(cfg.buffer_len)
+    nbuf = 4
+    stream, off = make_stream(pool, nbuf, left, right)
+    n_sym = cfg.buffer_len // 4
+    kw = dict(points=pool.points, labels=pool.labels, tone_bin=cfg.tbin, ref_pattern=pool.pattern, max_batch=nbuf)
+    ref = KKReceiver("CUSTOM", cfg.buffer_len, cfg.cspr_db, fir, pool.dc_offset, **kw)
+    out_ref = torch.empty(nbuf * n_sym, dtype=torch.uint8, device="cuda")
+    ref.submit_batch(torch.from_numpy(stream).cuda(), off, nbuf, out_ref)
+    c_ref = ref.sync()
+    packed = pack12(stream)
+    for src in (torch.from_numpy(packed).pin_memory(), torch.from_numpy(packed).cuda()):
+        r = KKReceiver("CUSTOM", cfg.buffer_len, cfg.cspr_db, fir, pool.dc_offset, **kw)
+        out = torch.empty(nbuf * n_sym, dtype=torch.uint8, device="cuda")
+        r.submit_batch_packed12(src, off, 3, out[:3 * n_sym])
+        r.submit_batch_packed12(src, off + 3 * cfg.buffer_len, 1, out[3 * n_sym:])
+        c = r.sync()
+        assert c == c_ref
+        assert torch.equal(out, out_ref)
+        r.close()
+    ref.close()

@@ -1,0 +1,30 @@
+"""Input formats (S0 ingest, no GPU): the packed 12-bit ADC byte format produced by
+synth.generate.pack12 round-trips through an independent bit-level unpacking, for
+the full 12-bit code range and random streams."""
+import numpy as np
+
+from synth.generate import pack12
+
+
+def _unpack_ref(b):
+    """bit-by-bit reference: sample k occupies bits [12k, 12k+12) of the little-endian byte stream"""
+    bits = np.unpackbits(np.asarray(b, dtype=np.uint8), bitorder="little")
+    n = bits.size // 12
+    v = bits[:12 * n].reshape(n, 12).astype(np.int64) @ (1 << np.arange(12))
+    return np.where(v >= 2048, v - 4096, v).astype(np.int16)
+
+
+def test_pack12_full_range_round_trip():
+    c = np.arange(-2048, 2048, dtype=np.int16)
+    p = pack12(c)
+    assert p.dtype == np.uint8 and p.size == c.size * 3 // 2
+    assert np.array_equal(_unpack_ref(p), c)
+
+
+def test_pack12_random_stream_and_layout():
+    rng = np.random.default_rng(3)
+    c = rng.integers(-2048, 2048, 10_000).astype(np.int16)
+    assert np.array_equal(_unpack_ref(pack12(c)), c)
+    # documented byte layout of one pair (include/kk_rx.h): c0 = 0xABC (-1348), c1 = 0x123
+    p = pack12(np.array([0xABC - 4096, 0x123], dtype=np.int16))
+    assert list(p) == [0xBC, 0x3A, 0x12]
