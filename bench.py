@@ -125,6 +125,20 @@ def measured_peaks():
         return {}
 
 
+def issue_limit(traffic, samples, launch_ms):
+    """The chain kernel against the SM issue rate (148 SMs x 4 schedulers x 1.965 GHz warp
+    instructions/s) with the warp-instruction count of the committed ncu capture
+    (DESIGN.md "Issue limit")."""
+    if not traffic or "chain_warp_inst_per_launch" not in traffic:
+        return None
+    ipsa = traffic["chain_warp_inst_per_launch"] / traffic["chain_samples_per_launch"]
+    peak = 148 * 4 * 1.965e9
+    bound = peak / ipsa / 1e9
+    achieved = samples / (launch_ms / 1e3) / 1e9
+    return {"warp_inst_per_sa": ipsa, "issue_bound_gsa": bound, "chain_gsa": achieved, "frac": achieved / bound,
+            "source": traffic.get("inst_source")}
+
+
 def profile_traffic():
     """dram bytes per kk_x2 launch from the committed `ncu --set full` capture."""
     try:
@@ -385,7 +399,8 @@ def run_gpu(args):
                      "flop_per_sa": FLOP_PER_SA_KERNEL, "samples_per_launch": B * N, "avg_launch_ms": ch_avg_ms,
                      "hbm_algorithmic_bytes_per_launch": HBM_BYTES_PER_SA * B * N,
                      "hbm_achieved_gbs": HBM_BYTES_PER_SA * B * N / (ch_avg_ms / 1e3) / 1e9,
-                     "peak_basis": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (derived, DESIGN.md)"},
+                     "peak_basis": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (derived, DESIGN.md)",
+                     "issue_limit": issue_limit(traffic, B * N, ch_avg_ms)},
         "kernel_ms_per_step": {"chain": ch_avg_ms, "lms_overlapped": lms_avg},
         "pipeline": ("kk_rx_submit_batch per step + one kk_rx_sync: the LMS update pass of batch j (one SM, "
                      "lane-per-chain) overlaps the fused chain of batch j-1, whose launch also computes batch j's "
