@@ -169,6 +169,22 @@ kk_status kk_rx_submit_batch_packed12(kk_rx_t *h, const uint8_t *first, int64_t 
  * *n_out (may be NULL).  Blocks until all outputs are valid. */
 kk_status kk_rx_sync(kk_rx_t *h, kk_rx_counts *out_per_buf, int64_t max_out, int64_t *n_out);
 
+/* Change the DC offset d (the offset lost by the AC-coupled ADC, swept offline)
+ * for subsequent submissions and calls; A_hat = sqrt(d c/(1+c)) follows (reading R6).
+ * Batches already submitted keep the offset they were submitted with.  KK_EINVAL if d <= 0. */
+kk_status kk_rx_set_dc_offset(kk_rx_t *h, float dc_offset);
+
+/* DC-offset sweep, the paper's measurement procedure (every measurement is
+ * repeated with different DC offsets, the best Q kept): the nbuf buffers at `first` (as in
+ * kk_rx_submit_batch) are processed once per offset dc_values[0..nd-1] (each a full S1-S7
+ * pass, back to back through the streaming pipeline; labels are not returned).
+ * out_per_dc: nd host structs (counters summed over the buffers) or NULL; *best: index of
+ * the lowest bit-error ratio (first on ties).  Drains pending submissions first; restores
+ * the handle's DC offset and advances the stream position by nbuf.  KK_EINVAL for bad
+ * arguments or non-positive offsets. */
+kk_status kk_rx_dc_sweep(kk_rx_t *h, const int16_t *first, int64_t nbuf, const float *dc_values, int nd,
+                         kk_rx_counts *out_per_dc, int *best);
+
 /* Kernel launches issued by submit/sync since the previous call of this function. */
 int64_t kk_rx_async_launches(kk_rx_t *h);
 

@@ -74,6 +74,9 @@ EXPORTS = {
     "kk_rx_submit_batch_packed12": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "kk_rx_sync": (C.c_int, [C.c_void_p, C.POINTER(KKCounts), C.c_int64, C.POINTER(C.c_int64)]),
     "kk_rx_async_launches": (C.c_int64, [C.c_void_p]),
+    "kk_rx_set_dc_offset": (C.c_int, [C.c_void_p, C.c_float]),
+    "kk_rx_dc_sweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_float), C.c_int,
+                                 C.POINTER(KKCounts), C.POINTER(C.c_int)]),
     "kk_rx_get_taps": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_float)]),
     "kk_rx_totals": (C.c_int, [C.c_void_p, C.POINTER(KKCounts)]),
     "kk_rx_reset_totals": (C.c_int, [C.c_void_p]),

@@ -50,6 +50,7 @@ struct Seg {
   const float2* taps;      // APPLY: [k][8]
   int64_t n_off;           // APPLY: pattern index of symbol 0 of owner owner_first
   const int16_t* codes;    // owner o's samples start at codes + o*N (halos readable)
+  float dc, a_hat;         // DC offset d and carrier amplitude A_hat of this segment's batch
 };
 
 // LMS update-pass look-up table (built on the host):

@@ -546,7 +546,6 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
   // CTA issues on sub-partition w % 4 and phase H leaves one role idle, so without the
   // rotation all four idle warps would share one sub-partition
   const int warp = ((tid >> 5) + gi) & (NWARPS - 1), lane = tid & 31;
-  const float invd = 1.0f / a.dc;
   const uint32_t n32 = (uint32_t)a.N;
   const int64_t ngroups = (int64_t)(gridDim.x - a.lms_ctas) * NGROUP, grp = (int64_t)blockIdx.x * NGROUP + gi;
   const int64_t T = a.total_steps;
@@ -641,6 +640,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     }
     const int16_t* obase = sg.codes + (int64_t)owner * a.N;
     const int64_t sbase = (int64_t)STEP * i - 256;   // owner position of stg[0] and ebuf[0]
+    const float invd = 1.0f / sg.dc;
     q_step = warm ? tone_index(a, sbase) : add_mod(q_step, s3072, n32);
     const int64_t wbase = (int64_t)STEP * i - 1280;  // owner position of wstg[0]
 
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           const int re0 = (int)(512 * c0 - 256 - base);
 #pragma unroll
           for (int j = 0; j < 48; ++j) {
-            const float vv = fmaxf((float)src[re0 + lane + 32 * j] + a.dc, a.vmin);
+            const float vv = fmaxf((float)src[re0 + lane + 32 * j] + sg.dc, a.vmin);
             // 0.5 ln 2 / 1024: the 1/1024 of the inverse FFT is folded in here
             const float l = lg2_ftz(vv * invd) * (0.34657359027997264f / 1024.0f);
             if (j < 32) v[brev(j, 5)].x = l;        // FFT input registers are bit-reversed
@@ -785,12 +785,12 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
             for (int hh = 0; hh < 2; ++hh) {
               const int o = 32 * t + 512 * hh;
               const float phi = dp0[o].y;
-              const float cv = (float)sp0[o] + a.dc;
+              const float cv = (float)sp0[o] + sg.dc;
               const float vv = fmaxf(cv, a.vmin);
               const float amp = vv * rsqrt_ftz(vv);
               float sp, cp;
               sincos_small(phi, &sp, &cp);  // |phi| of a few rad at most (KK phase)
-              dp0[o] = make_float2(fmaf(amp, cp, -a.a_hat), amp * sp);
+              dp0[o] = make_float2(fmaf(amp, cp, -sg.a_hat), amp * sp);
               clip += (cv < a.vmin && (allin || lane + 256 + o < lim)) ? 1u : 0u;
             }
           }

@@ -47,6 +47,7 @@ struct AsyncSlot {
   uint8_t* d_pack = nullptr;                // packed-12 input staging [1.5 (left + cap*N + right)]
   int64_t pack_cap = 0;
   int64_t nb = 0, index = 0, n_off0 = 0;
+  float dc = 0.f, a_hat = 0.f;              // DC offset hypothesis of the batch (kk_rx_set_dc_offset)
   const int16_t* codes = nullptr;           // device samples of buffer 0 of the batch
   uint8_t* out_dev = nullptr;               // where the chain writes labels
   uint8_t* out_host = nullptr;              // host destination (D2H after the chain) or NULL
@@ -64,6 +65,7 @@ struct kk_rx {
   int steps_per_buf = 0, pre_first = 0, pre_steps = 0;
   int64_t x2h = 0;
   float dc = 0, vmin = 1, a_hat = 0, mu = 1e-3f, tau = 0;
+  double cspr_lin = 1.0;                   // c = 10^(CSPR/10), for A_hat of a new DC offset
   int mode = 0;
   uint32_t tb_mod = 0, s32 = 0;
   int64_t P = 0, ref_offset = 0, stream_index = 0;
@@ -530,6 +532,7 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   h->vmin = p->v_min;
   const double c = std::pow(10.0, (double)cspr_db / 10.0);
   h->a_hat = (float)std::sqrt((double)p->dc_offset * c / (1.0 + c));  // reading R6
+  h->cspr_lin = c;
   h->mu = p->mu;
   h->tau = p->gate_tau < 0 ? (float)(dmin2 / 4.0) : p->gate_tau;
   h->mode = p->update_mode;
@@ -776,8 +779,8 @@ static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int
     ChainArgs ca{};
     fill_chain_common(h, ca, codes_dev);
     ca.nseg = 2;
-    ca.seg[0] = Seg{-1, 1, h->pre_first, S, SEG_X2_FULL, 0, 0, 0, x2f0, nullptr, nullptr, nullptr, 0, codes_dev};
-    ca.seg[1] = Seg{0, (int32_t)nb, 0, S, SEG_X2_FULL, count_clip, 0, 0, x2f0, nullptr, h->d_counts, nullptr, 0, codes_dev};
+    ca.seg[0] = Seg{-1, 1, h->pre_first, S, SEG_X2_FULL, 0, 0, 0, x2f0, nullptr, nullptr, nullptr, 0, codes_dev, h->dc, h->a_hat};
+    ca.seg[1] = Seg{0, (int32_t)nb, 0, S, SEG_X2_FULL, count_clip, 0, 0, x2f0, nullptr, h->d_counts, nullptr, 0, codes_dev, h->dc, h->a_hat};
     ca.es_dump = es;
     ca.total_steps = seg_steps(ca.seg[0]) + seg_steps(ca.seg[1]);
     CK(launch_chain(ca, h->grid_chain, h->stream));
@@ -790,7 +793,7 @@ static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int
     ChainArgs ca{};
     fill_chain_common(h, ca, codes_dev);
     ca.nseg = 1;
-    ca.seg[0] = Seg{-1, (int32_t)nb, h->pre_first, S, SEG_X2_TAIL, 0, 0, 0, h->d_tails, nullptr, nullptr, nullptr, 0, codes_dev};
+    ca.seg[0] = Seg{-1, (int32_t)nb, h->pre_first, S, SEG_X2_TAIL, 0, 0, 0, h->d_tails, nullptr, nullptr, nullptr, 0, codes_dev, h->dc, h->a_hat};
     ca.total_steps = seg_steps(ca.seg[0]);
     CK(launch_chain(ca, h->grid_chain, h->stream));
     h->last_launches += 1;
@@ -838,7 +841,7 @@ static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int
     ChainArgs ca{};
     fill_chain_common(h, ca, codes_dev);
     ca.nseg = 1;
-    ca.seg[0] = Seg{0, (int32_t)nb, 0, S, SEG_APPLY, 1, 0, 0, nullptr, out_dev, h->d_counts, h->d_taps, n_off0, codes_dev};
+    ca.seg[0] = Seg{0, (int32_t)nb, 0, S, SEG_APPLY, 1, 0, 0, nullptr, out_dev, h->d_counts, h->d_taps, n_off0, codes_dev, h->dc, h->a_hat};
     ca.total_steps = seg_steps(ca.seg[0]);
     CK(use_dyn(h, ca, h->stream));
     CK(launch_chain(ca, h->grid_chain, h->stream));
@@ -1079,7 +1082,7 @@ static kk_status issue_chain(kk_rx_t* h, int p, int t, const LmsArgs* la) {
   if (t >= 0) {
     AsyncSlot& at = h->aslot[t];
     ca.seg[ns++] = Seg{-1, (int32_t)at.nb, h->pre_first, S, SEG_X2_TAIL, 0, 0, 0, at.tails, nullptr, nullptr,
-                       nullptr, 0, at.codes};
+                       nullptr, 0, at.codes, at.dc, at.a_hat};
     ca.tail_ctr = h->d_ctr;
     ca.aligned16 = ca.aligned16 && ((uintptr_t)at.codes % 16) == 0;
     if (la) {  // batch t's update pass rides along as the last CTAs of this launch
@@ -1089,7 +1092,7 @@ static kk_status issue_chain(kk_rx_t* h, int p, int t, const LmsArgs* la) {
     }
   }
   ca.seg[ns++] = Seg{0, (int32_t)ap.nb, 0, S, SEG_APPLY, 1, 0, 0, nullptr, ap.out_dev, ap.d_counts, ap.taps, ap.n_off0,
-                     ap.codes};
+                     ap.codes, ap.dc, ap.a_hat};
   ca.nseg = ns;
   ca.total_steps = 0;
   for (int k = 0; k < ns; ++k) ca.total_steps += seg_steps(ca.seg[k]);
@@ -1157,6 +1160,8 @@ static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint
   if (st != KK_OK) return st;
   a.nb = nbuf;
   a.index = h->stream_index;
+  a.dc = h->dc;
+  a.a_hat = h->a_hat;
   const int64_t Pp = h->P;
   int64_t n_off0 = h->has_pattern ? ((h->ref_offset + (h->stream_index % Pp) * (h->n_sym % Pp)) % Pp) : 0;
   if (n_off0 < 0) n_off0 += Pp;
@@ -1219,7 +1224,7 @@ static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint
     fill_chain_common(h, ca, a.codes);
     ca.nseg = 1;
     ca.seg[0] = Seg{-1, (int32_t)nbuf, h->pre_first, h->steps_per_buf, SEG_X2_TAIL, 0, 0, 0, a.tails,
-                    nullptr, nullptr, nullptr, 0, a.codes};
+                    nullptr, nullptr, nullptr, 0, a.codes, a.dc, a.a_hat};
     ca.total_steps = seg_steps(ca.seg[0]);
     CK(launch_chain(ca, h->grid_chain, h->stream));
     // nothing else runs yet: the one-warp-per-chain kernel (lowest latency, many SMs)
@@ -1277,6 +1282,65 @@ extern "C" kk_status kk_rx_sync(kk_rx_t* h, kk_rx_counts* out_per_buf, int64_t m
     for (int64_t i = 0; i < n && i < max_out; ++i) out_per_buf[i] = h->a_counts[i];
   if (n_out) *n_out = n;
   h->a_counts.clear();
+  return KK_OK;
+}
+
+
+extern "C" kk_status kk_rx_set_dc_offset(kk_rx_t* h, float dc_offset) {
+  if (!h) return fail(KK_EINVAL, "null handle");
+  if (!(dc_offset > 0.f)) return fail(KK_EINVAL, "dc_offset must be > 0");
+  h->dc = dc_offset;
+  h->a_hat = (float)std::sqrt((double)dc_offset * h->cspr_lin / (1.0 + h->cspr_lin));  // reading R6
+  return KK_OK;
+}
+
+// "all measurements are performed multiple times using different DC offset
+// values" and the best Q is kept.  Each hypothesis is a full S1-S7 pass over the same
+// buffers; the hypotheses run back to back through the streaming pipeline.
+extern "C" kk_status kk_rx_dc_sweep(kk_rx_t* h, const int16_t* first, int64_t nbuf, const float* dc_values, int nd,
+                                    kk_rx_counts* out_per_dc, int* best) {
+  if (!h || !first || !dc_values || nd <= 0 || nbuf <= 0) return fail(KK_EINVAL, "bad arguments");
+  for (int k = 0; k < nd; ++k)
+    if (!(dc_values[k] > 0.f)) return fail(KK_EINVAL, "dc_values must be > 0");
+  const float dc0 = h->dc;
+  const int64_t idx0 = h->stream_index;
+  kk_status st = kk_rx_sync(h, nullptr, 0, nullptr);  // start from an empty pipeline
+  if (st != KK_OK) return st;
+  for (int k = 0; k < nd; ++k) {
+    kk_rx_set_dc_offset(h, dc_values[k]);
+    h->stream_index = idx0;
+    st = kk_rx_submit_batch(h, first, nbuf, nullptr);
+    if (st != KK_OK) break;
+  }
+  std::vector<kk_rx_counts> per((size_t)nd * nbuf);
+  int64_t n = 0;
+  if (st == KK_OK) st = kk_rx_sync(h, per.data(), (int64_t)per.size(), &n);
+  kk_rx_set_dc_offset(h, dc0);
+  h->stream_index = idx0 + nbuf;
+  if (st != KK_OK) return st;
+  if (n != (int64_t)nd * nbuf) return fail(KK_ECUDA, "dc sweep: unexpected result count");
+  int kb = 0;
+  double ber_b = 2.0;
+  for (int k = 0; k < nd; ++k) {
+    kk_rx_counts t{};
+    for (int64_t b = 0; b < nbuf; ++b) {
+      const kk_rx_counts& c = per[(size_t)k * nbuf + b];
+      t.bit_errors += c.bit_errors;
+      t.sym_errors += c.sym_errors;
+      t.bits += c.bits;
+      t.symbols += c.symbols;
+      t.clipped_samples += c.clipped_samples;
+      t.gated_updates += c.gated_updates;
+      t.flags |= c.flags;
+    }
+    if (out_per_dc) out_per_dc[k] = t;
+    const double ber = t.bits ? (double)t.bit_errors / (double)t.bits : 0.0;
+    if (ber < ber_b) {
+      ber_b = ber;
+      kb = k;
+    }
+  }
+  if (best) *best = kb;
   return KK_OK;
 }
 

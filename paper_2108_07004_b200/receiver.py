@@ -144,6 +144,21 @@ class KKReceiver:
         check(self._lib.kk_rx_sync(self.h, cnt, int(max_out), C.byref(n)), "kk_rx_sync")
         return [cnt[i].as_dict() for i in range(min(n.value, max_out))]
 
+    def set_dc_offset(self, dc_offset):
+        check(self._lib.kk_rx_set_dc_offset(self.h, float(dc_offset)), "kk_rx_set_dc_offset")
+
+    def dc_sweep(self, stream, offset, nbuf, dc_values):
+        """kk_rx_dc_sweep: counters (summed over the nbuf buffers) per DC offset and the
+        index of the best (lowest BER) offset."""
+        base, es = _ptr(stream)
+        assert es == 2
+        dv = np.ascontiguousarray(np.asarray(dc_values, dtype=np.float32))
+        cnt = (KKCounts * len(dv))()
+        best = C.c_int()
+        check(self._lib.kk_rx_dc_sweep(self.h, C.c_void_p(base + 2 * int(offset)), int(nbuf), _fptr(dv), len(dv),
+                                       cnt, C.byref(best)), "kk_rx_dc_sweep")
+        return [c.as_dict() for c in cnt], int(best.value)
+
     def async_launches(self):
         return int(self._lib.kk_rx_async_launches(self.h))
 

@@ -362,3 +362,50 @@ def test_packed12_input_equals_int16():
         assert torch.equal(out, out_ref)
         r.close()
     ref.close()
+
+
+def test_dc_offset_sweep():
+    """kk_rx_dc_sweep (measurements repeated over DC offsets, best Q kept):
+    the counters at the generator's offset equal a plain call bit for bit, an off-nominal
+    offset still meets the oracle parity contract (run with that offset), and the nominal
+    offset wins against +-30 %."""
+    _require_gpu()
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    name = "C2_n16"
+    cfg = configs.get(name).link
+    pool = make_pool(cfg, 2)
+    fir = _fir(name)
+    left, right = halo_for(cfg.buffer_len)
+    stream, off = make_stream(pool, 2, left, right)
+    src = torch.from_numpy(stream).cuda()
+    d0 = float(pool.dc_offset)
+    dvals = [0.7 * d0, d0, 1.3 * d0]
+    rx = KKReceiver(cfg.fmt, cfg.buffer_len, cfg.cspr_db, fir, d0, tone_bin=cfg.tbin, ref_pattern=pool.pattern)
+    per_dc, best = rx.dc_sweep(src, off, 2, dvals)
+    assert best == 1
+    bers = [c["bit_errors"] / c["bits"] for c in per_dc]
+    assert bers[1] <= bers[0] and bers[1] <= bers[2], bers
+    ref = KKReceiver(cfg.fmt, cfg.buffer_len, cfg.cspr_db, fir, d0, tone_bin=cfg.tbin, ref_pattern=pool.pattern)
+    c = ref.process_batch(src, off, 2)
+    assert per_dc[1]["bit_errors"] == sum(x["bit_errors"] for x in c)
+    assert per_dc[1]["sym_errors"] == sum(x["sym_errors"] for x in c)
+    # the off-nominal offset through the oracle (same float32 value on both sides)
+    d1 = float(np.float32(dvals[2]))
+    rx1 = KKReceiver(cfg.fmt, cfg.buffer_len, cfg.cspr_db, fir, d1, tone_bin=cfg.tbin, ref_pattern=pool.pattern,
+                     debug_dump=3, max_batch=2)
+    out = torch.empty(2 * (cfg.buffer_len // 4), dtype=torch.uint8, device="cuda")
+    counts = rx1.process_batch(src, off, 2, out)
+    n = cfg.buffer_len
+    win = stream[off - left: off + n + right]
+    p = O.RxParams(buffer_len=n, cspr_db=cfg.cspr_db, dc_offset=np.float32(d1), fir=fir, points=pool.points,
+                   labels=pool.labels, tone_bin=cfg.tbin, pattern=pool.pattern)
+    o = O.receive(win, left, p, want_stages=True)
+    x2_g = rx1.debug_x2(o["x2_first"], len(o["x2"]))
+    assert np.linalg.norm(x2_g - o["x2"]) / np.linalg.norm(o["x2"]) <= TOL_FIELD
+    inv = np.argsort(pool.labels)
+    dec_g = inv[out.cpu().numpy()[: n // 4].astype(np.int64)]
+    ok = o["margin"] >= EXEMPT
+    assert np.all(dec_g[ok] == o["decisions"][ok])
+    rx.close()
+    ref.close()
+    rx1.close()
