@@ -185,6 +185,32 @@ kk_status kk_rx_set_dc_offset(kk_rx_t *h, float dc_offset);
 kk_status kk_rx_dc_sweep(kk_rx_t *h, const int16_t *first, int64_t nbuf, const float *dc_values, int nd,
                          kk_rx_counts *out_per_dc, int *best);
 
+/* Init-time training (the static equaliser "is optimized offline using a
+ * training sequence every time that the data acquisition is initialized"; the adaptive
+ * equaliser converges "using a training sequence").  All three need an idle streaming
+ * pipeline (KK_ESTATE otherwise).
+ *
+ * kk_rx_train_fir: least-squares 203-tap static equaliser (reading R4) on ONE buffer
+ * (`buffer` as for kk_rx_process, device or host, halos readable) whose transmitted
+ * symbols [n_first, n_first + n_count) are known: symbols = 2*n_count floats (re, im).
+ * min_h sum_n |sum_t h_t E_s[4n + 101 - t] - s_n|^2 + ridge tr(R)/203 |h|^2, E_s from the
+ * GPU's S1-S3, normal equations and Cholesky solve in fp64 on the GPU.  Needs
+ * 4*n_first >= 101 and 4*(n_first+n_count-1)+101 < buffer_len.  out_fir: 2*203 floats
+ * (the layout of kk_rx_params.fir); not applied (see kk_rx_set_fir).
+ *
+ * kk_rx_set_fir: replace the static equaliser (2*203 floats; the EQ spectrum is recomputed
+ * in fp64 as at create).
+ *
+ * kk_rx_train_taps: the widely-linear taps after k_steps LMS steps in PILOT mode (known
+ * ref_pattern, from the handle's W_init and mu) over symbols [0, k_steps) of one buffer at
+ * the handle's stream position; out_w: 16 floats in the layout of kk_rx_params.w_init.
+ * KK_EINVAL without ref_pattern.  kk_rx_set_w_init installs such taps as W_init. */
+kk_status kk_rx_train_fir(kk_rx_t *h, const int16_t *buffer, const float *symbols, int64_t n_first, int64_t n_count,
+                          double ridge, float *out_fir);
+kk_status kk_rx_set_fir(kk_rx_t *h, const float *fir);
+kk_status kk_rx_train_taps(kk_rx_t *h, const int16_t *buffer, int32_t k_steps, float *out_w);
+kk_status kk_rx_set_w_init(kk_rx_t *h, const float *w);
+
 /* Kernel launches issued by submit/sync since the previous call of this function. */
 int64_t kk_rx_async_launches(kk_rx_t *h);
 

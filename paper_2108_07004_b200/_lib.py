@@ -75,6 +75,11 @@ EXPORTS = {
     "kk_rx_sync": (C.c_int, [C.c_void_p, C.POINTER(KKCounts), C.c_int64, C.POINTER(C.c_int64)]),
     "kk_rx_async_launches": (C.c_int64, [C.c_void_p]),
     "kk_rx_set_dc_offset": (C.c_int, [C.c_void_p, C.c_float]),
+    "kk_rx_train_fir": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_float), C.c_int64, C.c_int64, C.c_double,
+                                  C.POINTER(C.c_float)]),
+    "kk_rx_set_fir": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    "kk_rx_train_taps": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_float)]),
+    "kk_rx_set_w_init": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "kk_rx_dc_sweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_float), C.c_int,
                                  C.POINTER(KKCounts), C.POINTER(C.c_int)]),
     "kk_rx_get_taps": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_float)]),

@@ -1368,6 +1368,131 @@ cudaError_t launch_unpack12(const uint8_t* src, int16_t* dst, int64_t n_samples,
 }
 
 // ---------------------------------------------------------------------------
+// Init-time training of the static equaliser (NEXT row of SURVEY 8(f); PAPER l.53:
+// "optimized offline using a training sequence every time that the data acquisition
+// is initialized").  Least squares  min_h sum_n |sum_t h_t E_s[4n + 101 - t] - s_n|^2
+// (+ ridge), reading R4, in fp64: the normal equations R h = b with
+//   R[t1][t2] = sum_n conj(A[n][t1]) A[n][t2],  b[t] = sum_n conj(A[n][t]) s_n,
+//   A[n][t] = E_s[4 (n_first + n) + 101 - t],
+// accumulated by kk_gram_kernel (one 16 x 16 tile of R per CTA, the last tile row = b),
+// then solved by kk_chol_solve_kernel (one CTA, right-looking Cholesky, fp64).
+// ---------------------------------------------------------------------------
+constexpr int GRAM_T = 16;
+
+__global__ void __launch_bounds__(256) kk_gram_kernel(const float2* __restrict__ es, int64_t pos_first,
+                                                      const float2* __restrict__ sym, int n_count, int ntap,
+                                                      double2* __restrict__ R, double2* __restrict__ bvec) {
+  // tile (bx, by) of R; by == ceil(ntap/16) means the right-hand side b
+  const int t1 = blockIdx.y * GRAM_T + (threadIdx.x / GRAM_T);
+  const int t2 = blockIdx.x * GRAM_T + (threadIdx.x % GRAM_T);
+  const int nt = (ntap + GRAM_T - 1) / GRAM_T;
+  const bool rhs = (int)blockIdx.y == nt;
+  if (rhs && blockIdx.x > 0) return;
+  const int half = ntap / 2;
+  double sr = 0.0, si = 0.0;
+  if (!rhs && t1 < ntap && t2 < ntap && t2 >= t1) {
+    for (int n = 0; n < n_count; ++n) {
+      const int64_t base = pos_first + 4 * (int64_t)n + half;
+      const float2 a1 = es[base - t1], a2 = es[base - t2];
+      // conj(a1) * a2
+      sr += (double)a1.x * a2.x + (double)a1.y * a2.y;
+      si += (double)a1.x * a2.y - (double)a1.y * a2.x;
+    }
+    R[(int64_t)t1 * ntap + t2] = make_double2(sr, si);
+    R[(int64_t)t2 * ntap + t1] = make_double2(sr, -si);
+  } else if (rhs && threadIdx.x < GRAM_T) {
+    for (int t = threadIdx.x; t < ntap; t += GRAM_T) {
+      double br = 0.0, bi = 0.0;
+      for (int n = 0; n < n_count; ++n) {
+        const float2 a = es[pos_first + 4 * (int64_t)n + half - t];
+        const float2 s = sym[n];
+        br += (double)a.x * s.x + (double)a.y * s.y;
+        bi += (double)a.x * s.y - (double)a.y * s.x;
+      }
+      bvec[t] = make_double2(br, bi);
+    }
+  }
+}
+
+// (R + ridge * tr(R)/n * I) h = b, R Hermitian positive definite (n <= 256), in place;
+// one CTA of 256 threads, shared-memory-free (R in global / L2), fp64.
+__global__ void __launch_bounds__(256) kk_chol_solve_kernel(double2* __restrict__ R, double2* __restrict__ b, int n,
+                                                            double ridge, float* __restrict__ out) {
+  __shared__ double s_tr;
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int k = 0; k < n; ++k) tr += R[(int64_t)k * n + k].x;
+    s_tr = tr;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += blockDim.x) R[(int64_t)k * n + k].x += ridge * s_tr / n;
+  __syncthreads();
+  // Cholesky R = L L^H (lower triangle overwritten)
+  for (int k = 0; k < n; ++k) {
+    if (threadIdx.x == 0) {
+      const double d = sqrt(R[(int64_t)k * n + k].x);
+      R[(int64_t)k * n + k] = make_double2(d, 0.0);
+    }
+    __syncthreads();
+    const double inv = 1.0 / R[(int64_t)k * n + k].x;
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) {
+      double2 v = R[(int64_t)i * n + k];
+      R[(int64_t)i * n + k] = make_double2(v.x * inv, v.y * inv);
+    }
+    __syncthreads();
+    // trailing update R[i][j] -= L[i][k] conj(L[j][k]), j <= i
+    const int m = n - k - 1;
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+      const int i = k + 1 + idx / m, j = k + 1 + idx % m;
+      if (j > i) continue;
+      const double2 li = R[(int64_t)i * n + k], lj = R[(int64_t)j * n + k];
+      double2 r = R[(int64_t)i * n + j];
+      r.x -= li.x * lj.x + li.y * lj.y;
+      r.y -= li.y * lj.x - li.x * lj.y;
+      R[(int64_t)i * n + j] = r;
+    }
+    __syncthreads();
+  }
+  // forward L y = b, backward L^H h = y (one thread: n^2 operations)
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n; ++i) {
+      double2 s = b[i];
+      for (int j = 0; j < i; ++j) {
+        const double2 l = R[(int64_t)i * n + j], y = b[j];
+        s.x -= l.x * y.x - l.y * y.y;
+        s.y -= l.x * y.y + l.y * y.x;
+      }
+      const double d = R[(int64_t)i * n + i].x;
+      b[i] = make_double2(s.x / d, s.y / d);
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double2 s = b[i];
+      for (int j = i + 1; j < n; ++j) {
+        const double2 l = R[(int64_t)j * n + i], y = b[j];  // conj(L[j][i]) * h_j
+        s.x -= l.x * y.x + l.y * y.y;
+        s.y -= l.x * y.y - l.y * y.x;
+      }
+      const double d = R[(int64_t)i * n + i].x;
+      b[i] = make_double2(s.x / d, s.y / d);
+    }
+    for (int i = 0; i < n; ++i) {
+      out[2 * i] = (float)b[i].x;
+      out[2 * i + 1] = (float)b[i].y;
+    }
+  }
+}
+
+cudaError_t launch_train_fir(const float2* es, int64_t pos_first, const float2* sym, int n_count, int ntap, double ridge,
+                             double2* R, double2* b, float* out, cudaStream_t s) {
+  const int nt = (ntap + GRAM_T - 1) / GRAM_T;
+  kk_gram_kernel<<<dim3(nt, nt + 1), GRAM_T * GRAM_T, 0, s>>>(es, pos_first, sym, n_count, ntap, R, b);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  kk_chol_solve_kernel<<<1, 256, 0, s>>>(R, b, ntap, ridge, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Kernel 3: fixed-tap WL apply, decision, demap, count from materialised x2
 // (used when sub_block < buffer: several tap sets per buffer)
 // ---------------------------------------------------------------------------

@@ -69,6 +69,7 @@ struct kk_rx {
   int mode = 0;
   uint32_t tb_mod = 0, s32 = 0;
   int64_t P = 0, ref_offset = 0, stream_index = 0;
+  int64_t tone_bin = 0;
   bool has_pattern = false;
   uint32_t dump = 0;
   int grid_chain = 0;
@@ -316,6 +317,32 @@ static void build_lms_lut(const std::vector<double>& pts, int m, double tau, Lms
   if (n_fast) *n_fast = nf;
 }
 
+// S4 with the downconversion moved behind the LTI filter:
+//   x2[m] = e^{i theta_{2m}} sum_i h'_i D[2m - i],  h'_i = h_i e^{-2 pi i tb i / N}
+// Hs = DFT_1024(h' placed circularly) / 1024, fp64, rounded once (reading R16).
+static void eq_spectrum(const float* fir, int64_t tone_bin, int64_t buffer_len, float2* Hs) {
+  int64_t tbn = tone_bin % buffer_len;
+  if (tbn < 0) tbn += buffer_len;
+  std::vector<std::complex<double>> hp(203);
+  for (int t = 0; t < 203; ++t) {
+    const int64_t i = t - 101;
+    int64_t ph = (tbn * i) % buffer_len;
+    if (ph < 0) ph += buffer_len;
+    const double a = -2.0 * M_PI * (double)ph / (double)buffer_len;
+    hp[t] = std::complex<double>(fir[2 * t], fir[2 * t + 1]) * std::complex<double>(std::cos(a), std::sin(a));
+  }
+  for (int k = 0; k < 1024; ++k) {
+    std::complex<double> acc = 0;
+    for (int t = 0; t < 203; ++t) {
+      const int i = t - 101;
+      const double a = -2.0 * M_PI * (double)(((int64_t)k * (i + 1024)) % 1024) / 1024.0;
+      acc += hp[t] * std::complex<double>(std::cos(a), std::sin(a));
+    }
+    acc /= 1024.0;
+    Hs[k] = make_float2((float)acc.real(), (float)acc.imag());
+  }
+}
+
 extern "C" {
 
 int kk_rx_abi_version(void) { return KK_RX_ABI_VERSION; }
@@ -539,6 +566,7 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   int64_t tb = p->tone_bin % buffer_len;
   if (tb < 0) tb += buffer_len;
   h->tb_mod = (uint32_t)tb;
+  h->tone_bin = p->tone_bin;
   h->s32 = (uint32_t)((tb * 32) % buffer_len);
   h->has_pattern = p->ref_pattern != nullptr;
   h->P = h->has_pattern ? p->ref_len : 1;
@@ -560,28 +588,7 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   // S4 with the downconversion moved behind the LTI filter:
   //   x2[m] = e^{i theta_{2m}} sum_i h'_i D[2m - i],  h'_i = h_i e^{-2 pi i tb i / N}
   // Hs = DFT_1024(h' placed circularly) / 1024, fp64, rounded once (reading R16).
-  {
-    int64_t tbn = p->tone_bin % buffer_len;
-    if (tbn < 0) tbn += buffer_len;
-    std::vector<std::complex<double>> hp(203);
-    for (int t = 0; t < 203; ++t) {
-      const int64_t i = t - 101;
-      int64_t ph = (tbn * i) % buffer_len;
-      if (ph < 0) ph += buffer_len;
-      const double a = -2.0 * M_PI * (double)ph / (double)buffer_len;
-      hp[t] = std::complex<double>(p->fir[2 * t], p->fir[2 * t + 1]) * std::complex<double>(std::cos(a), std::sin(a));
-    }
-    for (int k = 0; k < 1024; ++k) {
-      std::complex<double> acc = 0;
-      for (int t = 0; t < 203; ++t) {
-        const int i = t - 101;
-        const double a = -2.0 * M_PI * (double)(((int64_t)k * (i + 1024)) % 1024) / 1024.0;
-        acc += hp[t] * std::complex<double>(std::cos(a), std::sin(a));
-      }
-      acc /= 1024.0;
-      Hs[k] = make_float2((float)acc.real(), (float)acc.imag());
-    }
-  }
+  eq_spectrum(p->fir, p->tone_bin, buffer_len, Hs.data());
   for (int k = 0; k < m; ++k) fpts[k] = make_float2((float)pts[2 * k], (float)pts[2 * k + 1]);
   if (p->w_init) {
     for (int k = 0; k < 8; ++k) winit[k] = make_float2(p->w_init[2 * k], p->w_init[2 * k + 1]);
@@ -1342,6 +1349,178 @@ extern "C" kk_status kk_rx_dc_sweep(kk_rx_t* h, const int16_t* first, int64_t nb
   }
   if (best) *best = kb;
   return KK_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Init-time training (NEXT row of SURVEY 8(f))
+// ---------------------------------------------------------------------------
+static bool pipeline_idle(const kk_rx_t* h) {
+  if (h->a_deferred >= 0) return false;
+  for (const AsyncSlot& a : h->aslot)
+    if (a.state != 0) return false;
+  return true;
+}
+
+// device copy (if needed) of one buffer + halos; returns the device pointer of its sample 0
+static kk_status stage_one(kk_rx_t* h, const int16_t* buffer, int16_t** tmp, const int16_t** dev0) {
+  *tmp = nullptr;
+  if (is_device_ptr(buffer)) {
+    *dev0 = buffer;
+    return KK_OK;
+  }
+  const size_t n = (size_t)(h->left + h->N + h->right);
+  CK(cudaMalloc(tmp, n * sizeof(int16_t)));
+  CK(cudaMemcpyAsync(*tmp, buffer - h->left, n * sizeof(int16_t), cudaMemcpyHostToDevice, h->stream));
+  *dev0 = *tmp + h->left;
+  return KK_OK;
+}
+
+// S1-S4 of one buffer with the debug outputs: x2 (index 0 <-> position 0, x2h samples of
+// margin before) and optionally E_s at positions [0, N)
+static kk_status one_buffer_stages(kk_rx_t* h, const int16_t* codes, float2* x2_full, float2* es) {
+  ChainArgs ca{};
+  fill_chain_common(h, ca, codes);
+  // the previous buffer's tail (x2 indices [-x2h, 0), from the left halo) and the buffer
+  ca.nseg = 2;
+  ca.seg[0] = Seg{-1, 1, h->pre_first, h->steps_per_buf, SEG_X2_FULL, 0, 0, 0, x2_full + h->x2h, nullptr, nullptr,
+                  nullptr, 0, codes, h->dc, h->a_hat};
+  ca.seg[1] = Seg{0, 1, 0, h->steps_per_buf, SEG_X2_FULL, 0, 0, 0, x2_full + h->x2h, nullptr, nullptr, nullptr, 0,
+                  codes, h->dc, h->a_hat};
+  ca.es_dump = es;
+  ca.total_steps = seg_steps(ca.seg[0]) + seg_steps(ca.seg[1]);
+  CK(launch_chain(ca, h->grid_chain, h->stream));
+  return KK_OK;
+}
+
+extern "C" kk_status kk_rx_train_fir(kk_rx_t* h, const int16_t* buffer, const float* symbols, int64_t n_first,
+                                     int64_t n_count, double ridge, float* out_fir) {
+  if (!h || !buffer || !symbols || !out_fir || n_count <= 0) return fail(KK_EINVAL, "bad arguments");
+  if (4 * n_first - 101 < 0 || 4 * (n_first + n_count - 1) + 101 >= h->N)
+    return fail(KK_EINVAL, "training symbols must satisfy 4*n_first >= 101 and 4*(n_first+n_count-1)+101 < buffer_len");
+  if (!pipeline_idle(h)) return fail(KK_ESTATE, "kk_rx_sync the streaming pipeline first");
+  CK(cudaSetDevice(h->device));
+  int16_t* tmp = nullptr;
+  const int16_t* dev0 = nullptr;
+  kk_status st = stage_one(h, buffer, &tmp, &dev0);
+  if (st != KK_OK) return st;
+  float2 *x2 = nullptr, *es = nullptr, *sym = nullptr;
+  double2 *R = nullptr, *b = nullptr;
+  float* out = nullptr;
+  auto release = [&]() {
+    void* ptrs[] = {tmp, x2, es, sym, R, b, out};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+  };
+  cudaError_t e = cudaSuccess;
+  const int ntap = 203;
+  if (e == cudaSuccess) e = cudaMalloc(&x2, (size_t)(h->x2h + h->N / 2 + 64) * sizeof(float2));
+  if (e == cudaSuccess) e = cudaMalloc(&es, (size_t)h->N * sizeof(float2));
+  if (e == cudaSuccess) e = cudaMalloc(&sym, (size_t)n_count * sizeof(float2));
+  if (e == cudaSuccess) e = cudaMalloc(&R, (size_t)ntap * ntap * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&b, (size_t)ntap * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&out, 2 * ntap * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(sym, symbols, (size_t)n_count * sizeof(float2), cudaMemcpyHostToDevice, h->stream);
+  if (e != cudaSuccess) {
+    release();
+    return fail(KK_ENOMEM, std::string("kk_rx_train_fir: ") + cudaGetErrorString(e));
+  }
+  st = one_buffer_stages(h, dev0, x2, es);
+  if (st == KK_OK) {
+    e = launch_train_fir(es, 4 * n_first, sym, (int)n_count, ntap, ridge, R, b, out, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_fir, out, 2 * ntap * sizeof(float), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) {
+      h->sticky = KK_ECUDA;
+      st = fail(KK_ECUDA, std::string("kk_rx_train_fir: ") + cudaGetErrorString(e));
+    }
+  }
+  release();
+  return st;
+}
+
+extern "C" kk_status kk_rx_set_fir(kk_rx_t* h, const float* fir) {
+  if (!h || !fir) return fail(KK_EINVAL, "bad arguments");
+  if (!pipeline_idle(h)) return fail(KK_ESTATE, "kk_rx_sync the streaming pipeline first");
+  CK(cudaSetDevice(h->device));
+  std::vector<float2> Hs(1024);
+  eq_spectrum(fir, h->tone_bin, h->N, Hs.data());
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaMemcpy(h->d_H, Hs.data(), 1024 * sizeof(float2), cudaMemcpyHostToDevice));
+  return KK_OK;
+}
+
+extern "C" kk_status kk_rx_set_w_init(kk_rx_t* h, const float* w) {
+  if (!h || !w) return fail(KK_EINVAL, "bad arguments");
+  if (!pipeline_idle(h)) return fail(KK_ESTATE, "kk_rx_sync the streaming pipeline first");
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaMemcpy(h->d_winit, w, 8 * sizeof(float2), cudaMemcpyHostToDevice));
+  return KK_OK;
+}
+
+// PAPER l.53 ("after initial setup and convergence using a training sequence"): the WL
+// taps after k_steps LMS steps in PILOT mode (known pattern) from the handle's W_init over
+// symbols [0, k_steps) of one buffer (stream position of the handle, as for process).
+extern "C" kk_status kk_rx_train_taps(kk_rx_t* h, const int16_t* buffer, int32_t k_steps, float* out_w) {
+  if (!h || !buffer || !out_w || k_steps <= 0) return fail(KK_EINVAL, "bad arguments");
+  if (!h->has_pattern) return fail(KK_EINVAL, "PILOT training needs ref_pattern");
+  if (4 * (int64_t)k_steps + 16 > h->N) return fail(KK_EINVAL, "k_steps must fit in the buffer");
+  if (!pipeline_idle(h)) return fail(KK_ESTATE, "kk_rx_sync the streaming pipeline first");
+  CK(cudaSetDevice(h->device));
+  int16_t* tmp = nullptr;
+  const int16_t* dev0 = nullptr;
+  kk_status st = stage_one(h, buffer, &tmp, &dev0);
+  if (st != KK_OK) return st;
+  float2 *x2 = nullptr, *taps = nullptr;
+  unsigned long long* cnt = nullptr;
+  cudaError_t e = cudaMalloc(&x2, (size_t)(h->x2h + h->N / 2 + 64) * sizeof(float2));
+  if (e == cudaSuccess) e = cudaMalloc(&taps, 8 * sizeof(float2));
+  if (e == cudaSuccess) e = cudaMalloc(&cnt, 8 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), h->stream);
+  if (e == cudaSuccess) {
+    st = one_buffer_stages(h, dev0, x2, nullptr);
+    if (st == KK_OK) {
+      const int64_t Pp = h->P;
+      int64_t idx0 = (h->ref_offset + (h->stream_index % Pp) * (h->n_sym % Pp)) % Pp;
+      if (idx0 < 0) idx0 += Pp;
+      LmsArgs la{};
+      la.lut = h->d_lmslut;
+      la.lcx = h->lms_lcx;
+      la.lcy = h->lms_lcy;
+      la.linv = h->lms_linv;
+      // one chain whose K update steps are symbols [0, K): the base is shifted by K symbols
+      la.x2_b0 = x2 + h->x2h + 2 * (int64_t)k_steps;
+      la.x2_stride = 0;
+      la.n_sym = h->n_sym;
+      la.L = h->n_sym;
+      la.nsub = 1;
+      la.nchains = 1;
+      la.K = k_steps;
+      la.mu = h->mu;
+      la.inv_tau = 0.f;
+      la.mode = KK_UPD_PILOT;
+      la.m = h->m;
+      la.pts = h->d_pts;
+      la.pattern = h->d_pattern;
+      la.P = Pp;
+      la.n_off0 = (idx0 + k_steps) % Pp;
+      la.w_init = h->d_winit;
+      la.taps = taps;
+      la.counts = cnt;
+      e = launch_lms(la, h->stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(out_w, taps, 8 * sizeof(float2), cudaMemcpyDeviceToHost, h->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    }
+  }
+  if (e != cudaSuccess && st == KK_OK) {
+    h->sticky = KK_ECUDA;
+    st = fail(KK_ECUDA, std::string("kk_rx_train_taps: ") + cudaGetErrorString(e));
+  }
+  void* ptrs[] = {tmp, x2, taps, cnt};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  return st;
 }
 
 extern "C" int64_t kk_rx_async_launches(kk_rx_t* h) {

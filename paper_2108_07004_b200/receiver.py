@@ -159,6 +159,38 @@ class KKReceiver:
                                        cnt, C.byref(best)), "kk_rx_dc_sweep")
         return [c.as_dict() for c in cnt], int(best.value)
 
+    def train_fir(self, stream, offset, symbols, n_first, ridge=1e-9):
+        """kk_rx_train_fir: LS 203-tap static equaliser from the buffer at `offset` whose
+        transmitted symbols n_first .. n_first+len(symbols)-1 are `symbols` (complex)."""
+        base, es = _ptr(stream)
+        assert es == 2
+        sy = np.asarray(symbols, dtype=np.complex128)
+        sf = np.ascontiguousarray(np.stack([sy.real, sy.imag], -1).reshape(-1).astype(np.float32))
+        out = np.empty(406, dtype=np.float32)
+        check(self._lib.kk_rx_train_fir(self.h, C.c_void_p(base + 2 * int(offset)), _fptr(sf), int(n_first), len(sy),
+                                        float(ridge), _fptr(out)), "kk_rx_train_fir")
+        return out[0::2] + 1j * out[1::2].astype(np.float64)
+
+    def set_fir(self, fir):
+        f = np.asarray(fir, dtype=np.complex128)
+        ff = np.ascontiguousarray(np.stack([f.real, f.imag], -1).reshape(-1).astype(np.float32))
+        check(self._lib.kk_rx_set_fir(self.h, _fptr(ff)), "kk_rx_set_fir")
+
+    def train_taps(self, stream, offset, k_steps):
+        """kk_rx_train_taps: (w[4], g[4]) after k_steps PILOT LMS steps on the buffer at `offset`."""
+        base, es = _ptr(stream)
+        assert es == 2
+        out = np.empty(16, dtype=np.float32)
+        check(self._lib.kk_rx_train_taps(self.h, C.c_void_p(base + 2 * int(offset)), int(k_steps), _fptr(out)),
+              "kk_rx_train_taps")
+        c = out[0::2] + 1j * out[1::2].astype(np.float64)
+        return c[:4], c[4:]
+
+    def set_w_init(self, w, g):
+        c = np.r_[np.asarray(w, dtype=np.complex128), np.asarray(g, dtype=np.complex128)]
+        ff = np.ascontiguousarray(np.stack([c.real, c.imag], -1).reshape(-1).astype(np.float32))
+        check(self._lib.kk_rx_set_w_init(self.h, _fptr(ff)), "kk_rx_set_w_init")
+
     def async_launches(self):
         return int(self._lib.kk_rx_async_launches(self.h))
 

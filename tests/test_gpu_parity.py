@@ -409,3 +409,54 @@ def test_dc_offset_sweep():
     rx.close()
     ref.close()
     rx1.close()
+
+
+def test_init_time_training():
+    """NEXT row of SURVEY 8(f): the LS static equaliser fitted on the GPU
+    (fp64 normal equations on the GPU's E_s) equals oracle.train.train_fir on the same
+    training window, and gives a noiseless buffer without errors once installed; the
+    PILOT-mode tap training equals the oracle's LMS in PILOT mode."""
+    _require_gpu()
+    from oracle import train
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    name = "C2_n16"
+    cfg = configs.get(name).link
+    n = cfg.buffer_len
+    left, right = halo_for(n)
+    # static equaliser from the noiseless training buffer
+    tr = make_pool(cfg, 1, noiseless=True, cache=False)
+    st, off = make_stream(tr, 1, left, right)
+    src = torch.from_numpy(st).cuda()
+    sym = tr.points[tr.pattern.astype(np.int64)]
+    n_first, n_count = 32, 8192
+    rx = KKReceiver(cfg.fmt, n, cfg.cspr_db, np.zeros(203), tr.dc_offset, tone_bin=cfg.tbin, ref_pattern=tr.pattern)
+    h_g = rx.train_fir(src, off, sym[n_first:n_first + n_count], n_first)
+    p = O.RxParams(buffer_len=n, cspr_db=cfg.cspr_db, dc_offset=tr.dc_offset, fir=np.zeros(O.FIR_TAPS),
+                   points=tr.points, labels=tr.labels, tone_bin=cfg.tbin)
+    h_o = train.train_fir(st, off, p, sym[n_first:n_first + n_count], n_first, n_count)
+    rel = np.linalg.norm(h_g - h_o) / np.linalg.norm(h_o)
+    assert rel < 2e-3, rel
+    rx.set_fir(h_g)
+    c = rx.process(src, off)
+    assert c["bit_errors"] == 0
+    rx.close()
+    # PILOT taps on a noisy buffer
+    pool = make_pool(cfg, 1)
+    fir = _fir(name)
+    st2, off2 = make_stream(pool, 1, left, right)
+    rx2 = KKReceiver(cfg.fmt, n, cfg.cspr_db, fir, pool.dc_offset, tone_bin=cfg.tbin, ref_pattern=pool.pattern)
+    K = 4096
+    w_g, g_g = rx2.train_taps(torch.from_numpy(st2).cuda(), off2, K)
+    p2 = O.RxParams(buffer_len=n, cspr_db=cfg.cspr_db, dc_offset=pool.dc_offset, fir=fir, points=pool.points,
+                    labels=pool.labels, tone_bin=cfg.tbin, pattern=pool.pattern)
+    o = O.receive(st2[off2 - left: off2 + n + right], left, p2, want_stages=True)
+    x2, x2_first = o["x2"], o["x2_first"]
+    w_o, g_o, _, _ = O.wl_lms_update(lambda m: x2[m - x2_first], 0, K, p2.w_init, p2.g_init, p2.mu, pool.points,
+                                     0.0, 1, pool.pattern, 0)
+    d = max(np.max(np.abs(w_g - w_o)), np.max(np.abs(g_g - g_o)))
+    assert d <= TOL_TAPS, d
+    # installing them as W_init is accepted and keeps the buffer decodable
+    rx2.set_w_init(w_g, g_g)
+    c2 = rx2.process(torch.from_numpy(st2).cuda(), off2)
+    assert c2["flags"] == 0
+    rx2.close()
