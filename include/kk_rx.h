@@ -211,6 +211,19 @@ kk_status kk_rx_set_fir(kk_rx_t *h, const float *fir);
 kk_status kk_rx_train_taps(kk_rx_t *h, const int16_t *buffer, int32_t k_steps, float *out_w);
 kk_status kk_rx_set_w_init(kk_rx_t *h, const float *w);
 
+/* GMI of constellations in complex AWGN (the GS optimiser's objective;
+ * SURVEY 8(f) NEXT-4), on the current CUDA device: standard BICM GMI (bits per symbol),
+ * Es = 1, N0 = 10^(-snr_db/10), expectation by 2-D Gauss-Hermite quadrature of `order`
+ * nodes per dimension.  points: n_cand * 2*m floats (re, im; candidate c at c*2*m),
+ * labels: n_cand * m bit labels (permutations of 0..m-1), m a power of two <= 256.
+ * out_gmi: n_cand doubles.  Blocking.  KK_EINVAL for bad arguments, KK_ECUDA. */
+kk_status kk_gmi_awgn(const float *points, const uint8_t *labels, int m, int n_cand, double snr_db, int order,
+                      double *out_gmi);
+
+/* Host only: Gauss-Hermite nodes and weights (weight e^{-t^2}, ascending nodes), Golub-Welsch.
+ * Returns order (1..64) or -1. */
+int kk_hermgauss(int order, double *nodes, double *weights);
+
 /* Kernel launches issued by submit/sync since the previous call of this function. */
 int64_t kk_rx_async_launches(kk_rx_t *h);
 

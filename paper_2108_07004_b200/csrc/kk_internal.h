@@ -155,6 +155,8 @@ int lms_lanes_ctas(int nchains);
 cudaError_t launch_apply(const ApplyArgs& a, cudaStream_t s);
 cudaError_t launch_train_fir(const float2* es, int64_t pos_first, const float2* sym, int n_count, int ntap, double ridge,
                              double2* R, double2* b, float* out, cudaStream_t s);
+cudaError_t launch_gmi(const float2* pts, const uint8_t* labs, int m, int nb, const double2* nodes, const double* wts,
+                       int nq, double n0, int n_cand, double* out, cudaStream_t s);
 cudaError_t launch_unpack12(const uint8_t* src, int16_t* dst, int64_t n_samples, cudaStream_t s);
 
 }  // namespace kk

@@ -1493,6 +1493,72 @@ cudaError_t launch_train_fir(const float2* es, int64_t pos_first, const float2* 
 }
 
 // ---------------------------------------------------------------------------
+// GMI of constellations in complex AWGN (NEXT row 4 of SURVEY 8(f); the
+// GS optimiser evaluates "the GMI for the AWGN channel" after every move).  Standard BICM
+// GMI, Es = 1, N0 = 10^(-SNR/10), expectation over the noise by 2-D
+// Gauss-Hermite quadrature (nodes t_a + i t_b, weights w_a w_b / pi):
+//   GMI = nb - (1/M) sum_k sum_q W_q sum_i log2( sum_j e^{-|y-p_j|^2/N0} /
+//                                                 sum_{j: b_i(j) = b_i(k)} e^{-|y-p_j|^2/N0} ),
+//   y = p_k + sqrt(N0) (t_a + i t_b).
+// One CTA per candidate constellation, one thread per (point k, node q); exponentials
+// shifted by the nearest point, sums and logs in fp64.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) kk_gmi_kernel(const float2* __restrict__ pts, const uint8_t* __restrict__ labs,
+                                                     int m, int nb, const double2* __restrict__ nodes,
+                                                     const double* __restrict__ wts, int nq, double n0,
+                                                     double* __restrict__ out) {
+  __shared__ float2 s_p[256];
+  __shared__ int s_l[256];
+  __shared__ double s_red[256];
+  const int c = blockIdx.x;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    s_p[j] = pts[(int64_t)c * m + j];
+    s_l[j] = labs[(int64_t)c * m + j];
+  }
+  __syncthreads();
+  const double sq = sqrt(n0), inv = 1.0 / n0;
+  double acc = 0.0;
+  for (int idx = threadIdx.x; idx < m * nq; idx += blockDim.x) {
+    const int k = idx / nq, q = idx - k * nq;
+    const double yx = (double)s_p[k].x + sq * nodes[q].x, yy = (double)s_p[k].y + sq * nodes[q].y;
+    double dmin = 1e300;
+    for (int j = 0; j < m; ++j) {
+      const double dx = yx - s_p[j].x, dy = yy - s_p[j].y;
+      dmin = fmin(dmin, dx * dx + dy * dy);
+    }
+    double den = 0.0, num[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int lk = s_l[k];
+    for (int j = 0; j < m; ++j) {
+      const double dx = yx - s_p[j].x, dy = yy - s_p[j].y;
+      const double e = exp(-(dx * dx + dy * dy - dmin) * inv);
+      den += e;
+      const int same = ~(s_l[j] ^ lk);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < nb && ((same >> i) & 1)) num[i] += e;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < nb) s += log2(den / num[i]);
+    acc += wts[q] * s;
+  }
+  s_red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) s_red[threadIdx.x] += s_red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[c] = (double)nb - s_red[0] / m;
+}
+
+cudaError_t launch_gmi(const float2* pts, const uint8_t* labs, int m, int nb, const double2* nodes, const double* wts,
+                       int nq, double n0, int n_cand, double* out, cudaStream_t s) {
+  kk_gmi_kernel<<<n_cand, 256, 0, s>>>(pts, labs, m, nb, nodes, wts, nq, n0, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Kernel 3: fixed-tap WL apply, decision, demap, count from materialised x2
 // (used when sub_block < buffer: several tap sets per buffer)
 // ---------------------------------------------------------------------------

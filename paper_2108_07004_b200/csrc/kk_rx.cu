@@ -1523,6 +1523,121 @@ extern "C" kk_status kk_rx_train_taps(kk_rx_t* h, const int16_t* buffer, int32_t
   return st;
 }
 
+
+// ---------------------------------------------------------------------------
+// GMI evaluation (NEXT row 4 of SURVEY 8(f)); host-side Gauss-Hermite nodes
+// ---------------------------------------------------------------------------
+// Gauss-Hermite nodes/weights (weight e^{-t^2}) by Golub-Welsch: eigen-decomposition of
+// the symmetric tridiagonal Jacobi matrix (diag 0, off-diag sqrt(k/2)) with implicit QL;
+// w_k = sqrt(pi) * v_{0k}^2.
+extern "C" int kk_hermgauss(int order, double* nodes, double* weights) {
+  if (order < 1 || order > 64 || !nodes || !weights) {
+    g_err = "order must be 1..64";
+    return -1;
+  }
+  const int n = order;
+  std::vector<double> d(n, 0.0), e(n, 0.0), z((size_t)n * n, 0.0);
+  for (int k = 1; k < n; ++k) e[k - 1] = std::sqrt(k / 2.0);
+  for (int k = 0; k < n; ++k) z[(size_t)k * n + k] = 1.0;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0, mm;
+    do {
+      for (mm = l; mm < n - 1; ++mm) {
+        const double dd = std::fabs(d[mm]) + std::fabs(d[mm + 1]);
+        if (std::fabs(e[mm]) <= 1e-16 * dd) break;
+      }
+      if (mm != l) {
+        if (iter++ == 60) break;
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = std::hypot(g, 1.0);
+        g = d[mm] - d[l] + e[l] / (g + (g >= 0 ? std::fabs(r) : -std::fabs(r)));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i;
+        for (i = mm - 1; i >= l; --i) {
+          double f = s * e[i], b = c * e[i];
+          r = std::hypot(f, g);
+          e[i + 1] = r;
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            e[mm] = 0.0;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          p = s * r;
+          d[i + 1] = g + p;
+          g = c * r - b;
+          for (int k = 0; k < n; ++k) {
+            f = z[(size_t)k * n + i + 1];
+            z[(size_t)k * n + i + 1] = s * z[(size_t)k * n + i] + c * f;
+            z[(size_t)k * n + i] = c * z[(size_t)k * n + i] - s * f;
+          }
+        }
+        if (r == 0.0 && i >= l) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[mm] = 0.0;
+      }
+    } while (mm != l);
+  }
+  std::vector<int> ord(n);
+  for (int k = 0; k < n; ++k) ord[k] = k;
+  std::sort(ord.begin(), ord.end(), [&](int a, int b) { return d[a] < d[b]; });
+  for (int k = 0; k < n; ++k) {
+    nodes[k] = d[ord[k]];
+    const double v = z[ord[k]];  // first component of eigenvector ord[k]
+    weights[k] = std::sqrt(M_PI) * v * v;
+  }
+  return n;
+}
+
+extern "C" kk_status kk_gmi_awgn(const float* points, const uint8_t* labels, int m, int n_cand, double snr_db, int order,
+                                 double* out_gmi) {
+  if (!points || !labels || !out_gmi || m < 2 || m > 256 || (m & (m - 1)) || n_cand < 1 || order < 1 || order > 64)
+    return fail(KK_EINVAL, "kk_gmi_awgn: bad arguments (m a power of two <= 256, order 1..64)");
+  int nb = 0;
+  while ((1 << nb) < m) ++nb;
+  if (nb > 8) return fail(KK_EINVAL, "kk_gmi_awgn: m > 256");
+  std::vector<double> t(order), w(order);
+  kk_hermgauss(order, t.data(), w.data());
+  std::vector<double2> nodes((size_t)order * order);
+  std::vector<double> wts((size_t)order * order);
+  for (int a = 0; a < order; ++a)
+    for (int b = 0; b < order; ++b) {
+      nodes[(size_t)a * order + b] = make_double2(t[a], t[b]);
+      wts[(size_t)a * order + b] = w[a] * w[b] / M_PI;
+    }
+  const double n0 = std::pow(10.0, -snr_db / 10.0);
+  const int nq = order * order;
+  float2* d_p = nullptr;
+  uint8_t* d_l = nullptr;
+  double2* d_n = nullptr;
+  double *d_w = nullptr, *d_o = nullptr;
+  kk_rx_t* h = nullptr;  // for CK()
+  auto release = [&]() {
+    void* ptrs[] = {d_p, d_l, d_n, d_w, d_o};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+  };
+  cudaError_t e = cudaMalloc(&d_p, (size_t)n_cand * m * sizeof(float2));
+  if (e == cudaSuccess) e = cudaMalloc(&d_l, (size_t)n_cand * m);
+  if (e == cudaSuccess) e = cudaMalloc(&d_n, (size_t)nq * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&d_w, (size_t)nq * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_o, (size_t)n_cand * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(d_p, points, (size_t)n_cand * m * sizeof(float2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_l, labels, (size_t)n_cand * m, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_n, nodes.data(), (size_t)nq * sizeof(double2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_w, wts.data(), (size_t)nq * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_gmi(d_p, d_l, m, nb, d_n, d_w, nq, n0, n_cand, d_o, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(out_gmi, d_o, (size_t)n_cand * sizeof(double), cudaMemcpyDeviceToHost);
+  release();
+  (void)h;
+  if (e != cudaSuccess) return fail(KK_ECUDA, std::string("kk_gmi_awgn: ") + cudaGetErrorString(e));
+  return KK_OK;
+}
+
 extern "C" int64_t kk_rx_async_launches(kk_rx_t* h) {
   if (!h) return 0;
   const int64_t n = h->a_launches;

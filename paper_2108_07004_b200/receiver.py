@@ -261,6 +261,30 @@ def builtin_constellation(fmt):
     return pts[0:2 * m:2] + 1j * pts[1:2 * m:2].astype(np.float64), lab[:m].astype(np.int64)
 
 
+def gmi_awgn(points, labels, snr_db, order=10):
+    """kk_gmi_awgn: GMI (bits/symbol) of one constellation, or of a batch when points is
+    [n_cand, m] and labels [n_cand, m]; returns a float or an array."""
+    lib = _lib.load()
+    pts = np.asarray(points, dtype=np.complex128)
+    single = pts.ndim == 1
+    pts = pts.reshape(-1, pts.shape[-1])
+    lab = np.ascontiguousarray(np.asarray(labels, dtype=np.uint8).reshape(pts.shape))
+    pf = np.ascontiguousarray(np.stack([pts.real, pts.imag], -1).reshape(-1).astype(np.float32))
+    out = np.empty(pts.shape[0], dtype=np.float64)
+    check(lib.kk_gmi_awgn(_fptr(pf), _u8ptr(lab), pts.shape[1], pts.shape[0], float(snr_db), int(order),
+                          out.ctypes.data_as(C.POINTER(C.c_double))), "kk_gmi_awgn")
+    return float(out[0]) if single else out
+
+
+def hermgauss(order):
+    lib = _lib.load()
+    t = np.empty(order, dtype=np.float64)
+    w = np.empty(order, dtype=np.float64)
+    if lib.kk_hermgauss(int(order), t.ctypes.data_as(C.POINTER(C.c_double)), w.ctypes.data_as(C.POINTER(C.c_double))) < 0:
+        raise ValueError(order)
+    return t, w
+
+
 def halo_for(buffer_len, k_update=4096):
     lib = _lib.load()
     l, r = C.c_int64(), C.c_int64()

@@ -460,3 +460,28 @@ def test_init_time_training():
     c2 = rx2.process(torch.from_numpy(st2).cuda(), off2)
     assert c2["flags"] == 0
     rx2.close()
+
+
+def test_gmi_matches_oracle():
+    """NEXT row 4 of SURVEY 8(f): kk_gmi_awgn (BICM GMI in AWGN by Gauss-Hermite
+    quadrature, one CTA per candidate) equals oracle.shaping.gmi_awgn, single and batched."""
+    _require_gpu()
+    from oracle import shaping
+    from paper_2108_07004_b200 import gmi_awgn
+    from synth.generate import load_constellation
+    cases = [("QAM16", 14.0, 10), ("GS8", 14.0, 10), ("QAM8", 10.0, 10), ("QAM128", 20.0, 6), ("GS128", 20.0, 6),
+             ("QAM64", 18.0, 8)]
+    for fmt, snr, order in cases:
+        p, l = load_constellation(fmt)
+        g = gmi_awgn(p, l, snr, order)
+        o = shaping.gmi_awgn(p, l, snr, order)
+        assert abs(g - o) <= 2e-5, (fmt, g, o)
+    # batch: label-swapped variants of QAM16 in one launch
+    p, l = load_constellation("QAM16")
+    rng = np.random.default_rng(5)
+    L = np.stack([l] + [rng.permutation(l) for _ in range(7)])
+    P = np.stack([p] * 8)
+    g = gmi_awgn(P, L, 12.0, 10)
+    o = np.array([shaping.gmi_awgn(p, L[i], 12.0, 10) for i in range(8)])
+    assert np.max(np.abs(g - o)) <= 2e-5
+    assert g[0] == g.max()  # Gray labelling is the best of these

@@ -28,3 +28,19 @@ def test_pack12_random_stream_and_layout():
     # documented byte layout of one pair (include/kk_rx.h): c0 = 0xABC (-1348), c1 = 0x123
     p = pack12(np.array([0xABC - 4096, 0x123], dtype=np.int16))
     assert list(p) == [0xBC, 0x3A, 0x12]
+
+
+def test_hermgauss_exactness():
+    """kk_hermgauss (host, Golub-Welsch): the n-node rule integrates t^(2j) e^(-t^2)
+    exactly (= Gamma(j + 1/2)) for 2j <= 2n - 1, odd moments vanish; nodes/weights equal
+    numpy's rule."""
+    import math
+    from paper_2108_07004_b200 import hermgauss
+    for n in (1, 2, 6, 10, 20):
+        t, w = hermgauss(n)
+        assert np.all(np.diff(t) > 0) and np.all(w > 0)
+        for j in range(n):
+            assert abs(np.sum(w * t ** (2 * j)) - math.gamma(j + 0.5)) <= 1e-12 * max(1.0, math.gamma(j + 0.5))
+            assert abs(np.sum(w * t ** (2 * j + 1))) <= 1e-11 * max(1.0, math.gamma(j + 1.0))
+        t0, w0 = np.polynomial.hermite.hermgauss(n)
+        assert np.max(np.abs(t - t0)) < 1e-12 and np.max(np.abs(w - w0)) < 1e-12
