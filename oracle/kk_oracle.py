@@ -60,6 +60,30 @@ UPD_DD_SOFT, UPD_PILOT, UPD_DD_HARD = 0, 1, 2
 # ----------------------------------------------------------------------------
 # O1 / S1 front end
 # ----------------------------------------------------------------------------
+def pre_equalize(codes, d, g):
+    """Pre-KK static equaliser (PAPER l.167 [chenKKFE]): a short real
+    FIR on the detected intensity before sqrt/log, undoing the PD/ADC roll-off,
+        v'[n] = sum_{k=-h..h} g_k (code[n - k] + d),   g_k = g[k + h],  len(g) = 2h + 1.
+    Plain direct convolution; returns v' for n = h .. len(codes)-1-h (length len - 2h)."""
+    v = np.asarray(codes, dtype=np.float64) + np.float64(d)
+    g = np.asarray(g, dtype=np.float64)
+    h = (len(g) - 1) // 2
+    assert len(g) == 2 * h + 1
+    n = len(v) - 2 * h
+    out = np.zeros(n, dtype=np.float64)
+    for k in range(-h, h + 1):
+        out += g[k + h] * v[h - k: h - k + n]
+    return out
+
+
+def frontend_v(v, v_min=1.0):
+    """S1 on intensities already holding the DC offset: clamp, sqrt, log."""
+    v = np.asarray(v, dtype=np.float64)
+    clipped = v < v_min
+    v = np.maximum(v, np.float64(v_min))
+    return np.sqrt(v), 0.5 * np.log(v), clipped
+
+
 def frontend(codes, d, v_min=1.0):
     """v = max(code + d, v_min); a = sqrt(v); l = ln a = 0.5 ln v.
 
@@ -330,6 +354,7 @@ class RxParams:
     v_min: float = 1.0
     pattern: np.ndarray | None = None   # ref indices (error-count reference)
     ref_offset: int = 0
+    pre_fir: np.ndarray | None = None   # real [2h+1], pre-KK intensity equaliser (NEXT-3), h <= 8
 
 
 def d_min(points):
@@ -366,11 +391,19 @@ def receive(window, left, p: RxParams, want_stages=False):
     K = int(p.k_update)
     window = np.asarray(window)
     right = len(window) - left - n_buf
-    if left < required_left(K) or right < required_right():
-        raise ValueError("window too small: need left>=%d right>=%d" % (required_left(K), required_right()))
+    hp = 0 if p.pre_fir is None else (len(p.pre_fir) - 1) // 2
+    if left < required_left(K) + hp or right < required_right() + hp:
+        raise ValueError("window too small: need left>=%d right>=%d" % (required_left(K) + hp, required_right() + hp))
     pos0 = -left
-    # S1
-    a, l, clipped = frontend(window, p.dc_offset, p.v_min)
+    # S1 (with the optional pre-KK intensity equaliser: the window loses h samples per side)
+    if p.pre_fir is not None:
+        h = (len(p.pre_fir) - 1) // 2
+        a, l, clipped = frontend_v(pre_equalize(window, p.dc_offset, p.pre_fir), p.v_min)
+        window = window[h:len(window) - h]
+        left -= h
+        pos0 = -left
+    else:
+        a, l, clipped = frontend(window, p.dc_offset, p.v_min)
     # S2 on every whole chunk the window supports
     j_first = -(-(pos0 + HILBERT_DISCARD) // HILBERT_HOP)
     j_last = (pos0 + len(window) - (HILBERT_NFFT - HILBERT_DISCARD)) // HILBERT_HOP

@@ -45,3 +45,18 @@ def train_fir(window, left, p: O.RxParams, symbols_tx, n_first, n_count, ridge=1
     AhA += ridge * np.trace(AhA).real / O.FIR_TAPS * np.eye(O.FIR_TAPS)
     h = np.linalg.solve(AhA, A.conj().T @ b)
     return h
+
+
+def train_prefir(window, target, d, h, ridge=1e-9):
+    """Pre-KK intensity equaliser: real taps g[0..2h] minimising
+    sum_n |sum_k g_k (window[n - k] + d) - (target[n] + d)|^2 (+ ridge) over the
+    interior of the window; `target` = the same buffer's codes without the PD/ADC
+    roll-off (the noiseless training pair of synth.generate)."""
+    v = np.asarray(window, dtype=np.float64) + np.float64(d)
+    t = np.asarray(target, dtype=np.float64) + np.float64(d)
+    n = len(v) - 2 * h
+    A = np.stack([v[h - k: h - k + n] for k in range(-h, h + 1)], axis=1)
+    b = t[h: h + n]
+    AtA = A.T @ A
+    AtA += ridge * np.trace(AtA) / (2 * h + 1) * np.eye(2 * h + 1)
+    return np.linalg.solve(AtA, A.T @ b)

@@ -79,6 +79,7 @@ class LinkConfig:
     seed_pat: int = 1
     seed_noise: int = 1000
     adc_bits: int = 12
+    adc_bw_hz: float | None = None   # PD + ADC bandwidth (Gaussian, 3 dB at adc_bw_hz); None = ideal
 
     @property
     def n_sym(self):
@@ -200,6 +201,17 @@ def _noise_intensity(cfg, e_clean, rng):
     raise ValueError(cfg.noise)
 
 
+def adc_filter(intens, bw_hz):
+    """Finite PD + ADC bandwidth on the detected intensity (the paper's 1 GHz ADC,
+    PAPER l.68; error-floor mechanism l.70, l.167): Gaussian low-pass |H(f)| =
+    exp(-(ln 2 / 2) (f / bw)^2) (3 dB at bw), circular over each buffer period."""
+    x = np.atleast_2d(np.asarray(intens, dtype=np.float64))
+    f = sfft.rfftfreq(x.shape[-1], d=1 / FS)
+    hf = np.exp(-0.5 * np.log(2.0) * (f / bw_hz) ** 2)
+    y = sfft.irfft(sfft.rfft(x, axis=-1, workers=-1) * hf, n=x.shape[-1], axis=-1, workers=-1)
+    return y.reshape(np.shape(intens))
+
+
 def adc_gain(cfg: LinkConfig, i_clean=None):
     """Deterministic ADC gain: the noiseless swing fills +-(2^(b-1)-1) times an
     analytic headroom of 4 sigma of the signal-ASE beat term (function of the
@@ -250,6 +262,8 @@ def make_pool(cfg: LinkConfig, n_pool: int = 1, cache: bool = True, noiseless: b
         seqs = np.random.SeedSequence(cfg.seed_noise).spawn(n_pool)
         for b in range(n_pool):
             intens[b] = _noise_intensity(cfg, e_clean, np.random.Generator(np.random.PCG64(seqs[b])))
+    if cfg.adc_bw_hz is not None:
+        intens = adc_filter(intens, cfg.adc_bw_hz)
     full = 2 ** (cfg.adc_bits - 1) - 1
     mean_i = float(intens.mean())
     codes = np.clip(np.rint(gain * (intens - mean_i)), -(full + 1), full).astype(np.int16)

@@ -426,3 +426,76 @@ def test_closed_form_ber_reductions():
     ber = O.count_errors(dec, idx, labs)["bit_errors"] / (6 * n)
     th = Mx.ber_square_qam_gray(64, snr)
     assert abs(ber - th) < 4 * np.sqrt(th / (6 * n)) + 0.02 * th
+
+
+# ----------------------------------------------------------------------------
+# pre-KK intensity equaliser
+# ----------------------------------------------------------------------------
+def test_pre_equalize_identity_constant_and_delay():
+    from oracle import kk_oracle as O
+    rng = np.random.default_rng(11)
+    c = rng.integers(-2048, 2048, 4000)
+    d = 1234.5
+    g = np.zeros(15)
+    g[7] = 1.0
+    assert np.array_equal(O.pre_equalize(c, d, g), c[7:-7] + d)          # identity
+    g2 = np.zeros(15)
+    g2[9] = 1.0                                                            # k = +2: v'[n] = v[n - 2]
+    assert np.array_equal(O.pre_equalize(c, d, g2), c[5:-9] + d)
+    k = np.array([0.1, -0.3, 1.4, -0.3, 0.1])
+    assert np.allclose(O.pre_equalize(np.full(50, 7), d, k), (7 + d) * k.sum())  # DC gain
+
+
+def test_pre_equalize_identity_receive_unchanged():
+    """receive() with the identity pre-equaliser equals receive() without it."""
+    from oracle import kk_oracle as O
+    from synth import configs
+    from synth.generate import make_pool, make_stream
+    wl = configs.get("C2_n16")
+    cfg = wl.link
+    pool = make_pool(cfg, 1, cache=False)
+    h = np.loadtxt("data/fir/C2_n16.txt")
+    fir = h[:, 0] + 1j * h[:, 1]
+    left, right = O.required_left(4096) + 8, O.required_right() + 8
+    st, off = make_stream(pool, 1, left, right)
+    kw = dict(buffer_len=cfg.buffer_len, cspr_db=cfg.cspr_db, dc_offset=pool.dc_offset, fir=fir, points=pool.points,
+              labels=pool.labels, tone_bin=cfg.tbin, pattern=pool.pattern)
+    a = O.receive(st, off, O.RxParams(**kw))
+    g = np.zeros(9)
+    g[4] = 1.0
+    b = O.receive(st, off, O.RxParams(pre_fir=g, **kw))
+    assert np.array_equal(a["decisions"], b["decisions"]) and a["bit_errors"] == b["bit_errors"]
+    assert np.max(np.abs(a["y"] - b["y"])) == 0.0
+
+
+def test_pre_equalizer_lowers_the_bandwidth_error_floor():
+    """With a 1 GHz PD/ADC bandwidth (the error-floor mechanism of l.70/l.167)
+    the noiseless EVM degrades; the LS-trained pre-KK equaliser (oracle.train.train_prefir,
+    trained on the filtered/unfiltered noiseless pair) recovers most of it."""
+    from dataclasses import replace
+    from oracle import kk_oracle as O
+    from oracle import train
+    from synth.generate import LinkConfig, make_pool, make_stream
+    cfg0 = LinkConfig("QAM16", 14.0, None, "one_sided", 1 << 16, seed_noise=77)
+    cfg1 = replace(cfg0, adc_bw_hz=1.0e9)
+    p0 = make_pool(cfg0, 1, cache=False)
+    p1 = make_pool(cfg1, 1, cache=False)
+    h = np.loadtxt("data/fir/C2_n16.txt")
+    fir = h[:, 0] + 1j * h[:, 1]
+    hp = 7
+    left, right = O.required_left(4096) + hp, O.required_right() + hp
+    s0, off = make_stream(p0, 1, left, right)
+    s1, _ = make_stream(p1, 1, left, right)
+    g = train.train_prefir(s1, s0, p1.dc_offset, hp)
+    kw = dict(buffer_len=cfg1.buffer_len, cspr_db=cfg1.cspr_db, fir=fir, points=p1.points, labels=p1.labels,
+              tone_bin=cfg1.tbin, pattern=p1.pattern)
+    sym = p1.points[p1.pattern.astype(np.int64)]
+
+    def evm(st, d, pre):
+        o = O.receive(st, off, O.RxParams(dc_offset=d, pre_fir=pre, **kw))
+        return 10 * np.log10(np.mean(np.abs(o["y"] - sym) ** 2) / np.mean(np.abs(sym) ** 2))
+    e_ideal = evm(s0, p0.dc_offset, None)
+    e_bw = evm(s1, p1.dc_offset, None)
+    e_eq = evm(s1, p1.dc_offset, g)
+    assert e_bw > e_ideal + 3.0          # the roll-off raises the floor
+    assert e_eq < e_bw - 3.0             # the pre-KK equaliser removes most of it
