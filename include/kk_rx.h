@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define KK_RX_ABI_VERSION 1
+#define KK_RX_ABI_VERSION 2
 
 typedef struct kk_rx kk_rx_t; /* opaque: owns device scratch, tables, streams */
 
@@ -87,6 +87,11 @@ typedef struct {
   void *cuda_stream;        /* cudaStream_t to launch on, NULL = handle-owned stream */
   uint32_t debug_dump;      /* bitmask of KK_DUMP_* */
   int32_t max_batch;        /* buffers per internal batch (device scratch sizing), default 16 */
+  /* ABI 2: pre-KK intensity equaliser: real taps g_k,
+   * k = -h..h, h = (pre_fir_len-1)/2 <= 8, applied before sqrt/log:
+   * v' = sum_k g_k (code[n-k] + d).  NULL = off. */
+  const float *pre_fir;
+  int32_t pre_fir_len;
 } kk_rx_params;
 
 /* Per-buffer (or aggregate) counters, "Error counting". */

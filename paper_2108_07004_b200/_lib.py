@@ -43,6 +43,8 @@ class KKParams(C.Structure):
         ("cuda_stream", C.c_void_p),
         ("debug_dump", C.c_uint32),
         ("max_batch", C.c_int32),
+        ("pre_fir", C.POINTER(C.c_float)),
+        ("pre_fir_len", C.c_int32),
     ]
 
 

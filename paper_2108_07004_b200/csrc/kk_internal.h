@@ -16,6 +16,9 @@ constexpr int EQ_KEEP = 768;
 constexpr int EBUF = STEP + 256;    // D = E_tf - A_hat window of one step: [3072 i - 256, 3072 i + 3072)
 constexpr int STG = STEP + 512;     // codes of one step: [3072 i - 256, 3072 i + 3328)
 constexpr int WARM = 1536;          // warm-up codes: [3072 i - 1280, 3072 i + 256)
+constexpr int PKH = 8;              // extra codes staged per side (pre-KK equaliser reach, <= 8)
+constexpr int STG2 = STG + 2 * PKH;   // staged codes of one step: [3072 i - 256 - PKH, ...)
+constexpr int WARM2 = WARM + 2 * PKH; // staged warm-up codes
 constexpr int XS = 1538;            // x2 window of one step (APPLY): positions 3072 i - 132 + 2 j
 constexpr int NWARPS = 4;          // warps per group
 constexpr int NGROUP = 4;          // independent groups per CTA (one CTA per SM)
@@ -51,6 +54,7 @@ struct Seg {
   int64_t n_off;           // APPLY: pattern index of symbol 0 of owner owner_first
   const int16_t* codes;    // owner o's samples start at codes + o*N (halos readable)
   float dc, a_hat;         // DC offset d and carrier amplitude A_hat of this segment's batch
+  float prek_dsum;         // d * sum(pre-KK taps) (pre-KK equaliser only)
 };
 
 // LMS update-pass look-up table (built on the host):
@@ -121,6 +125,10 @@ struct ChainArgs {
   // blocks; lane-per-chain body, waits on tail_ctr for the tails this launch computes)
   int32_t lms_ctas, lms_mode;
   LmsArgs lms;
+  // pre-KK intensity equaliser: v' = sum_{k=-h..h} prek[k+h] code[n-k] + dsum,
+  // dsum = d * sum(prek) per segment (Seg.prek_dsum); prek_h < 0: off (the plain kernel)
+  int32_t prek_h;
+  float prek[2 * PKH + 1];
   // diagnostics (KKRX_PHASE_TIMING): per-group clock64 sums [0] staging, [1] phase H,
   // [2] phase E, [3] phase A + step tail, [4] steps, [5] H task busy (3 warps), [6] E task busy (4 warps)
   unsigned long long* dbg;

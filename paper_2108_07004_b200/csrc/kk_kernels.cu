@@ -38,14 +38,16 @@ constexpr size_t SMEM_TW512 = 512 * sizeof(float2);   // 512-pt twiddles
 constexpr size_t SMEM_LUT = 64 * 64 * sizeof(uint32_t);  // decision table (g <= 64)
 constexpr size_t SMEM_SHARED = SMEM_TW + SMEM_H + SMEM_TW512 + SMEM_LUT;
 constexpr size_t SMEM_EBUF = EBUF * sizeof(float2);
-constexpr size_t SMEM_STG = STG * sizeof(int16_t);
+constexpr size_t SMEM_STG = STG2 * sizeof(int16_t);
+static_assert(SMEM_STG % 16 == 0 && (PKH * 2) % 16 == 0, "bulk copies of the staged codes stay 16-B aligned");
 constexpr size_t SMEM_XS = XS * sizeof(float2);  // also holds the warm-up codes (WARM int16)
 constexpr size_t SMEM_PAT = 832;                 // pattern bytes of one step (768 + alignment)
 constexpr size_t SMEM_GROUP = SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT + 64 + 16;  // + factored WL taps + mbarriers
 constexpr size_t CHAIN_SMEM = SMEM_SHARED + NGROUP * SMEM_GROUP;
 static_assert(SMEM_GROUP % 16 == 0 && SMEM_SHARED % 16 == 0, "16-B aligned regions");
 static_assert(LMS_LUT_G * LMS_LUT_G * 8 + 129 * 8 <= SMEM_SHARED + NGROUP * SMEM_GROUP, "LMS CTAs fit the chain smem");
-static_assert(WARM * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-up codes + tile must fit the x2 window");
+static_assert(WARM2 * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-up codes + tile must fit the x2 window");
+constexpr int WOFF = WARM2 * (int)sizeof(int16_t) / (int)sizeof(float2);  // float2 offset of the warm-up tile in xs
 static_assert(TILE * sizeof(float) <= EQ_KEEP * sizeof(float2), "transpose tile must fit an EQ stride of ebuf");
 
 size_t chain_smem_bytes() { return CHAIN_SMEM; }
@@ -226,6 +228,18 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned b
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// v = code + d at staged index q, or with the pre-KK intensity equaliser (SURVEY 8(f)
+// NEXT-3) v' = sum_{k=-h..h} g_k code[q - k] + d sum(g) (taps as kernel-parameter operands)
+template <bool PREKK>
+__device__ __forceinline__ float prek_v(const ChainArgs& a, const int16_t* src, int q, const Seg& sg) {
+  if (!PREKK) return (float)src[q] + sg.dc;
+  float v = sg.prek_dsum;
+#pragma unroll
+  for (int k = -PKH; k <= PKH; ++k)
+    if (k >= -a.prek_h && k <= a.prek_h) v = fmaf(a.prek[k + PKH], (float)src[q - k], v);
+  return v;
 }
 
 struct StepPos {
@@ -496,6 +510,7 @@ __global__ void __launch_bounds__(LMSL_MAXW * 32) kk_lms_lanes_kernel(LmsArgs a)
 //   phase E: 4 static-EQ blocks (one per warp): S4 -> x2 (smem or HBM)
 //   phase A: 768 symbols of S5' + S6 + S7 (APPLY segments)
 // ---------------------------------------------------------------------------
+template <bool PREKK>
 __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(ChainArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (a.lms_ctas > 0 && (int)blockIdx.x >= (int)gridDim.x - a.lms_ctas) {
@@ -516,7 +531,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
   float2* xs = reinterpret_cast<float2*>(gbase + SMEM_EBUF + SMEM_STG);
   uint8_t* spat = gbase + SMEM_EBUF + SMEM_STG + SMEM_XS;
   int16_t* wstg = reinterpret_cast<int16_t*>(xs);  // warm-up codes (H phase only)
-  float* wscr = reinterpret_cast<float*>(xs + WARM / 4);  // warm-up task's transpose tile
+  float* wscr = reinterpret_cast<float*>(xs + WOFF);  // warm-up task's transpose tile
   float2* s_taps = reinterpret_cast<float2*>(gbase + SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT);  // ta[4], tc[4]
   uint64_t* bar = reinterpret_cast<uint64_t*>(gbase + SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT + 64);
   uint64_t* pbar = bar + 1;
@@ -650,19 +665,19 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
       mbar_wait(bar, phase_bit);
       phase_bit ^= 1u;
     } else if (a.aligned16) {
-      const uint4* s4 = reinterpret_cast<const uint4*>(obase + sbase);
+      const uint4* s4 = reinterpret_cast<const uint4*>(obase + sbase - PKH);
       uint4* d4 = reinterpret_cast<uint4*>(stg);
-      for (int k = tid; k < STG / 8; k += NWARPS * 32) d4[k] = __ldg(s4 + k);
+      for (int k = tid; k < STG2 / 8; k += NWARPS * 32) d4[k] = __ldg(s4 + k);
     } else {
-      for (int k = tid; k < STG; k += NWARPS * 32) stg[k] = obase[sbase + k];
+      for (int k = tid; k < STG2; k += NWARPS * 32) stg[k] = obase[sbase - PKH + k];
     }
     if (warm) {
       if (a.aligned16) {
-        const uint4* s4 = reinterpret_cast<const uint4*>(obase + wbase);
+        const uint4* s4 = reinterpret_cast<const uint4*>(obase + wbase - PKH);
         uint4* d4 = reinterpret_cast<uint4*>(wstg);
-        for (int k = tid; k < WARM / 8; k += NWARPS * 32) d4[k] = __ldg(s4 + k);
+        for (int k = tid; k < WARM2 / 8; k += NWARPS * 32) d4[k] = __ldg(s4 + k);
       } else {
-        for (int k = tid; k < WARM; k += NWARPS * 32) wstg[k] = obase[wbase + k];
+        for (int k = tid; k < WARM2; k += NWARPS * 32) wstg[k] = obase[wbase - PKH + k];
       }
     }
     // pattern bytes of this step's symbols (APPLY with counting): bulk copy, waited for in phase A
@@ -708,7 +723,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
         prefetched = next_cont && a.aligned16;
         if (prefetched && tid == 0) {
           fence_proxy_async();
-          bulk_load(stg, obase + sbase + STEP, STG * sizeof(int16_t), bar);
+          bulk_load(stg, obase + sbase + STEP - PKH, STG2 * sizeof(int16_t), bar);
         }
       }
       const bool active = !isH || warp < 3 || warm;
@@ -724,7 +739,8 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           const int re0 = (int)(512 * c0 - 256 - base);
 #pragma unroll
           for (int j = 0; j < 48; ++j) {
-            const float vv = fmaxf((float)src[re0 + lane + 32 * j] + sg.dc, a.vmin);
+            const int q = PKH + re0 + lane + 32 * j;
+            const float vv = fmaxf(prek_v<PREKK>(a, src, q, sg), a.vmin);
             // 0.5 ln 2 / 1024: the 1/1024 of the inverse FFT is folded in here
             const float l = lg2_ftz(vv * invd) * (0.34657359027997264f / 1024.0f);
             if (j < 32) v[brev(j, 5)].x = l;        // FFT input registers are bit-reversed
@@ -764,7 +780,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           const int s_off = (int)(512 * c0 - 256 - base);
           const int e_off = (int)(512 * c0 - 256 - sbase);
           // warm-up task: all 1024 outputs to a slice of xs (its tile is dead), then its last 256 to ebuf[0, 256)
-          float2* dst = wt ? (xs + WARM / 4 - 256) : (ebuf + e_off);
+          float2* dst = wt ? (xs + WOFF - 256) : (ebuf + e_off);
           const bool cnt = !wt && sg.count_clip && (mode == SEG_APPLY || owner >= sg.ref);
           const int lim = (int)((a.N - sbase < (int64_t)(1 << 30)) ? a.N - sbase : (int64_t)(1 << 30)) - e_off;
           unsigned clip = 0;
@@ -776,7 +792,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
             dst[lane + 32 * n2 + 512].y = -v[n2].y;
           }
           // outputs mm = lane + 256 + 32 t (chunk c0) and mm + 512 (chunk c0 + 1), t = 0..15
-          const int16_t* sp0 = src + s_off + lane + 256;
+          const int16_t* sp0 = src + PKH + s_off + lane + 256;
           float2* dp0 = dst + lane + 256;
           const bool allin = lim >= 1280;  // every output position of this task is < N
 #pragma unroll 2
@@ -785,7 +801,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
             for (int hh = 0; hh < 2; ++hh) {
               const int o = 32 * t + 512 * hh;
               const float phi = dp0[o].y;
-              const float cv = (float)sp0[o] + sg.dc;
+              const float cv = PREKK ? prek_v<true>(a, sp0, o, sg) : (float)sp0[o] + sg.dc;
               const float vv = fmaxf(cv, a.vmin);
               const float amp = vv * rsqrt_ftz(vv);
               float sp, cp;
@@ -999,9 +1015,11 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
 cudaError_t chain_setup(int device, int* grid_out) {
   int sms = 0, occ = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  cudaError_t e = cudaFuncSetAttribute(kk_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM);
+  cudaError_t e = cudaFuncSetAttribute(kk_chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kk_chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM);
   if (e != cudaSuccess) return e;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk_chain_kernel, NGROUP * NWARPS * 32, CHAIN_SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk_chain_kernel<false>, NGROUP * NWARPS * 32, CHAIN_SMEM);
   if (occ < 1) occ = 1;
   *grid_out = sms * occ;
   return cudaGetLastError();
@@ -1010,7 +1028,10 @@ cudaError_t chain_setup(int device, int* grid_out) {
 cudaError_t launch_chain(const ChainArgs& a, int grid, cudaStream_t s) {
   if (a.total_steps <= 0) return cudaSuccess;
   if (grid > a.total_steps) grid = (int)a.total_steps;
-  kk_chain_kernel<<<grid, NGROUP * NWARPS * 32, CHAIN_SMEM, s>>>(a);
+  if (a.prek_h >= 0)
+    kk_chain_kernel<true><<<grid, NGROUP * NWARPS * 32, CHAIN_SMEM, s>>>(a);
+  else
+    kk_chain_kernel<false><<<grid, NGROUP * NWARPS * 32, CHAIN_SMEM, s>>>(a);
   return cudaGetLastError();
 }
 

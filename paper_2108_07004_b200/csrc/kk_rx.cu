@@ -66,6 +66,9 @@ struct kk_rx {
   int64_t x2h = 0;
   float dc = 0, vmin = 1, a_hat = 0, mu = 1e-3f, tau = 0;
   double cspr_lin = 1.0;                   // c = 10^(CSPR/10), for A_hat of a new DC offset
+  int prek_h = -1;                         // pre-KK equaliser half length (-1: off)
+  float prek[2 * PKH + 1] = {0};
+  double prek_sum = 0.0;
   int mode = 0;
   uint32_t tb_mod = 0, s32 = 0;
   int64_t P = 0, ref_offset = 0, stream_index = 0;
@@ -145,8 +148,9 @@ static void halo_geometry(int64_t N, int K, int64_t* left, int64_t* right, int* 
   // method needs (oracle window): 512*ceil((4K+4+101)/512) + 256 and 768
   const int64_t need = 4 * (int64_t)K + 4 + 101;
   const int64_t m_left = 512 * ((need + 511) / 512) + 256;
-  *left = std::max(gpu_left, m_left);
-  *right = std::max<int64_t>(gpu_right, 768);
+  // + PKH: the kernel stages PKH extra codes per side (pre-KK equaliser reach)
+  *left = std::max(gpu_left, m_left) + PKH;
+  *right = std::max<int64_t>(gpu_right, 768) + PKH;
   if (spb) *spb = steps;
   if (i0) *i0 = first;
   if (x2h) *x2h = X2H;
@@ -483,6 +487,8 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   if (!(p->dc_offset > 0.f)) return fail(KK_EINVAL, "dc_offset must be > 0");
   if (!(p->v_min > 0.f)) return fail(KK_EINVAL, "v_min must be > 0");
   if (p->max_batch < 0) return fail(KK_EINVAL, "max_batch must be >= 0");
+  if (p->pre_fir && (p->pre_fir_len < 1 || p->pre_fir_len > 2 * PKH + 1 || p->pre_fir_len % 2 == 0))
+    return fail(KK_EINVAL, "pre_fir_len must be odd and <= 17");
 
   // constellation
   std::vector<double> pts;
@@ -560,6 +566,13 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   const double c = std::pow(10.0, (double)cspr_db / 10.0);
   h->a_hat = (float)std::sqrt((double)p->dc_offset * c / (1.0 + c));  // reading R6
   h->cspr_lin = c;
+  if (p->pre_fir) {
+    h->prek_h = (p->pre_fir_len - 1) / 2;
+    for (int k = 0; k < p->pre_fir_len; ++k) {
+      h->prek[PKH - h->prek_h + k] = p->pre_fir[k];
+      h->prek_sum += (double)p->pre_fir[k];
+    }
+  }
   h->mu = p->mu;
   h->tau = p->gate_tau < 0 ? (float)(dmin2 / 4.0) : p->gate_tau;
   h->mode = p->update_mode;
@@ -706,6 +719,8 @@ static bool is_device_ptr(const void* p) {
 
 static void fill_chain_common(kk_rx_t* h, ChainArgs& ca, const int16_t* codes_dev) {
   ca.N = h->N;
+  ca.prek_h = h->prek_h;
+  for (int k = 0; k < 2 * PKH + 1; ++k) ca.prek[k] = h->prek[k];
   ca.dbg = h->d_dbg;
   ca.x2h = h->x2h;
   ca.dc = h->dc;
@@ -734,6 +749,12 @@ static void fill_chain_common(kk_rx_t* h, ChainArgs& ca, const int16_t* codes_de
 }
 
 static int64_t seg_steps(const Seg& g) { return (int64_t)g.n_own * (g.i_end - g.i_begin); }
+
+// every chain launch: d * sum(pre-KK taps) per segment (each segment may carry its own d)
+static cudaError_t chain_launch(const kk_rx_t* h, ChainArgs& ca, int grid, cudaStream_t st) {
+  for (int k = 0; k < ca.nseg; ++k) ca.seg[k].prek_dsum = (float)((double)ca.seg[k].dc * h->prek_sum);
+  return launch_chain(ca, grid, st);
+}
 
 // dynamic work distribution for one chain launch: a zeroed counter from the ring
 // (slot 0 is the async pipeline's tail counter)
@@ -790,7 +811,7 @@ static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int
     ca.seg[1] = Seg{0, (int32_t)nb, 0, S, SEG_X2_FULL, count_clip, 0, 0, x2f0, nullptr, h->d_counts, nullptr, 0, codes_dev, h->dc, h->a_hat};
     ca.es_dump = es;
     ca.total_steps = seg_steps(ca.seg[0]) + seg_steps(ca.seg[1]);
-    CK(launch_chain(ca, h->grid_chain, h->stream));
+    CK(chain_launch(h, ca, h->grid_chain, h->stream));
     h->last_launches += 1;
     return KK_OK;
   };
@@ -802,7 +823,7 @@ static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int
     ca.nseg = 1;
     ca.seg[0] = Seg{-1, (int32_t)nb, h->pre_first, S, SEG_X2_TAIL, 0, 0, 0, h->d_tails, nullptr, nullptr, nullptr, 0, codes_dev, h->dc, h->a_hat};
     ca.total_steps = seg_steps(ca.seg[0]);
-    CK(launch_chain(ca, h->grid_chain, h->stream));
+    CK(chain_launch(h, ca, h->grid_chain, h->stream));
     h->last_launches += 1;
   } else {
     kk_status st = full_pass(1, h->d_es);
@@ -851,7 +872,7 @@ static kk_status run_chunk(kk_rx_t* h, const int16_t* codes_dev, int64_t nb, int
     ca.seg[0] = Seg{0, (int32_t)nb, 0, S, SEG_APPLY, 1, 0, 0, nullptr, out_dev, h->d_counts, h->d_taps, n_off0, codes_dev, h->dc, h->a_hat};
     ca.total_steps = seg_steps(ca.seg[0]);
     CK(use_dyn(h, ca, h->stream));
-    CK(launch_chain(ca, h->grid_chain, h->stream));
+    CK(chain_launch(h, ca, h->grid_chain, h->stream));
   } else {
     ApplyArgs aa{};
     aa.x2 = x2f0;
@@ -1111,7 +1132,7 @@ static kk_status issue_chain(kk_rx_t* h, int p, int t, const LmsArgs* la) {
     CK(e);
   }
   if (h->timing) CK(cudaEventRecord(ap.ev_t[2], h->stream));
-  CK(launch_chain(ca, grid, h->stream));
+  CK(chain_launch(h, ca, grid, h->stream));
   if (h->timing) CK(cudaEventRecord(ap.ev_t[3], h->stream));
   ap.timed_chain = h->timing;
   h->a_launches += 1;
@@ -1233,7 +1254,7 @@ static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint
     ca.seg[0] = Seg{-1, (int32_t)nbuf, h->pre_first, h->steps_per_buf, SEG_X2_TAIL, 0, 0, 0, a.tails,
                     nullptr, nullptr, nullptr, 0, a.codes, a.dc, a.a_hat};
     ca.total_steps = seg_steps(ca.seg[0]);
-    CK(launch_chain(ca, h->grid_chain, h->stream));
+    CK(chain_launch(h, ca, h->grid_chain, h->stream));
     // nothing else runs yet: the one-warp-per-chain kernel (lowest latency, many SMs)
     if (h->timing) CK(cudaEventRecord(a.ev_t[0], h->stream));
     CK(launch_lms(la, h->stream));
@@ -1389,7 +1410,7 @@ static kk_status one_buffer_stages(kk_rx_t* h, const int16_t* codes, float2* x2_
                   codes, h->dc, h->a_hat};
   ca.es_dump = es;
   ca.total_steps = seg_steps(ca.seg[0]) + seg_steps(ca.seg[1]);
-  CK(launch_chain(ca, h->grid_chain, h->stream));
+  CK(chain_launch(h, ca, h->grid_chain, h->stream));
   return KK_OK;
 }
 

@@ -37,7 +37,7 @@ class KKReceiver:
 
     def __init__(self, fmt, buffer_len, cspr_db, fir, dc_offset, *, points=None, labels=None, tone_bin=541065,
                  w_init=None, mu=1e-3, k_update=4096, sub_block=0, gate_tau=-1.0, update_mode=0, ref_pattern=None,
-                 ref_offset=0, v_min=1.0, device=-1, stream=None, debug_dump=0, max_batch=16):
+                 ref_offset=0, v_min=1.0, device=-1, stream=None, debug_dump=0, max_batch=16, pre_fir=None):
         lib = _lib.load()
         self._lib = lib
         p = KKParams()
@@ -79,6 +79,11 @@ class KKReceiver:
         p.cuda_stream = stream
         p.debug_dump = debug_dump
         p.max_batch = max_batch
+        if pre_fir is not None:
+            pf = np.ascontiguousarray(np.asarray(pre_fir, dtype=np.float32))
+            self._keep.append(pf)
+            p.pre_fir = _fptr(pf)
+            p.pre_fir_len = len(pf)
         fmt_id = _lib.FORMATS[fmt] if isinstance(fmt, str) else int(fmt)
         h = C.c_void_p()
         check(lib.kk_rx_create(C.byref(h), fmt_id, 4, int(buffer_len), float(cspr_db), C.byref(p)), "kk_rx_create")

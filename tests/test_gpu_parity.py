@@ -485,3 +485,28 @@ def test_gmi_matches_oracle():
     o = np.array([shaping.gmi_awgn(p, L[i], 12.0, 10) for i in range(8)])
     assert np.max(np.abs(g - o)) <= 2e-5
     assert g[0] == g.max()  # Gray labelling is the best of these
+
+
+def test_pre_kk_equaliser_parity():
+    """NEXT row 3 of SURVEY 8(f): the pre-KK intensity equaliser (15 taps, trained by
+    oracle.train.train_prefir on the noiseless filtered/unfiltered pair) on a link with a
+    1 GHz PD/ADC bandwidth, noisy: the full parity contract against oracle.receive(pre_fir)."""
+    _require_gpu()
+    from dataclasses import replace
+    from oracle import train
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    cfg0 = LinkConfig("QAM16", 14.0, None, "one_sided", 1 << 16, seed_noise=91)
+    t0 = make_pool(cfg0, 1, cache=False)
+    t1 = make_pool(replace(cfg0, adc_bw_hz=1.0e9), 1, cache=False)
+    left, right = halo_for(cfg0.buffer_len)
+    s0, off0 = make_stream(t0, 1, left, right)
+    s1, _ = make_stream(t1, 1, left, right)
+    g = train.train_prefir(s1, s0, t1.dc_offset, 7)
+    cfg = replace(cfg0, osnr_db=20.0, adc_bw_hz=1.0e9)
+    pool = make_pool(cfg, 2)
+    fir = _fir("C2_n16")
+    gp = _gpu_run(pool, cfg, fir, 2, pre_fir=np.float32(g))
+    for b in range(2):
+        o = _oracle(gp["stream"], gp["off"], b, cfg, pool, fir, gp["left"], gp["right"], pre_fir=np.float32(g).astype(np.float64))
+        rep = _check_buffer(gp, o, b, cfg, pool)
+        print("prekk", b, rep)

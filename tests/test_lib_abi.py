@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol(root):
     for n in names:
         assert hasattr(lib, n), n
         assert n in _lib.EXPORTS, f"binding misses {n}"
-    assert lib.kk_rx_abi_version() == 1
+    assert lib.kk_rx_abi_version() == 2
 
 
 def test_builtin_constellations_match_data_files(root):
@@ -70,4 +70,4 @@ def test_halo_covers_method_needs():
     for n in (1 << 16, 1 << 22, 66048):
         left, right = halo_for(n, 4096)
         assert left >= O.required_left(4096) and right >= O.required_right()
-    assert halo_for(1 << 22, 4096) == (17664, 2304)
+    assert halo_for(1 << 22, 4096) == (17672, 2312)
