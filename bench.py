@@ -317,6 +317,35 @@ def run_gpu(args):
     samples_total = world * args.steps * B * N
     value = samples_total / (ms_max / 1e3) / 1e9
 
+    # ---------------- cuFFT comparison (north star: "cuFFT reported only as a comparison";
+    # SURVEY 8(d)): S1-S4 of the same batches as a multi-kernel pipeline around cuFFT with
+    # every intermediate in HBM (libkkrx_cufft.so).  It stops at x2; the fused chain above
+    # also runs S5-S7.  Rank 0 at N = 1 only.
+    cufft_cmp = None
+    if world == 1 and not args.no_cufft:
+        from paper_2108_07004_b200.cufft_cmp import CufftS1S4
+        cm = CufftS1S4(N, B, pool.dc_offset, cfg.cspr_db, fir, tone_bin=cfg.tbin)
+        x2_out = torch.empty(B * (N // 2), dtype=torch.complex64, device=dev)
+        for s in range(args.warmup):
+            cm.x2(d_stream, off + first_buf(s) * N, B, x2_out, cur.cuda_stream)
+        torch.cuda.synchronize(dev)
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        c0.record(cur)
+        for s in range(args.steps):
+            cm.x2(d_stream, off + first_buf(s) * N, B, x2_out, cur.cuda_stream)
+        c1.record(cur)
+        torch.cuda.synchronize(dev)
+        cms = c0.elapsed_time(c1)
+        cv = args.steps * B * N / (cms / 1e3) / 1e9
+        cufft_cmp = {"value": cv, "unit": UNIT, "ms_per_step": cms / args.steps, "stages": "S1-S4 (to x2)",
+                     "launches_per_step": cm.launches(B),
+                     "design": "pack -> cuFFT C2C 1024 -> mask -> cuFFT C2C 1024 -> S3 (E_s to HBM) -> cuFFT C2C "
+                               "1024 over overlapping windows -> x H + fold -> cuFFT C2C 512 -> extract",
+                     "fused_full_chain_over_cufft_s1_s4": value / cv}
+        del x2_out
+        cm.close()
+
     # ---------------- e2e through the same C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -412,6 +441,8 @@ def run_gpu(args):
     }
     if e2e:
         line["e2e"] = e2e
+    if cufft_cmp:
+        line["cufft_comparison"] = cufft_cmp
     if world == 1 and not args.no_cpu_baseline:
         workers = args.ref_workers or (os.cpu_count() or 1)
         v, dt, s = oracle_rate(args.workload, P, workers, workers)
@@ -436,6 +467,7 @@ def main():
     ap.add_argument("--ref-workers", type=int, default=0, help="oracle processes (0 = all host cores)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cufft", action="store_true", help="skip the cuFFT comparison leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: W >= 3

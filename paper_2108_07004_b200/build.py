@@ -14,6 +14,27 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v", "-I", os.path.join(os.path.dirname(HERE), "include")]
 SOURCES = ["kk_rx.cu", "kk_kernels.cu", "kk_constellation.cpp"]
+# comparison only (include/kk_cufft_cmp.h): the cuFFT multi-kernel S1-S4 pipeline
+CMP_OUT = os.path.join(HERE, "libkkrx_cufft.so")
+CMP_SOURCES = ["kk_cufft_cmp.cu"]
+CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
+
+
+def build_cmp(verbose=False, force=False):
+    """libkkrx_cufft.so: the cuFFT comparison pipeline (never the product path)."""
+    srcs = [os.path.join(CSRC, s) for s in CMP_SOURCES]
+    deps = srcs + [os.path.join(os.path.dirname(HERE), "include", "kk_cufft_cmp.h")]
+    if not force and os.path.exists(CMP_OUT) and all(os.path.getmtime(CMP_OUT) >= os.path.getmtime(d) for d in deps):
+        return CMP_OUT
+    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", CMP_OUT + ".tmp", *srcs, "-cudart", "static",
+           "-L", CUDA_LIB, "-lcufft", "-Xlinker", "-rpath=" + CUDA_LIB]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+    if r.returncode != 0:
+        raise RuntimeError("nvcc failed (%d)" % r.returncode)
+    os.replace(CMP_OUT + ".tmp", CMP_OUT)
+    return CMP_OUT
 
 
 def build(verbose=False, force=False, out=None, csrc=None, include=None):
@@ -42,3 +63,4 @@ def build(verbose=False, force=False, out=None, csrc=None, include=None):
 
 if __name__ == "__main__":
     print(build(verbose=True, force="--force" in sys.argv))
+    print(build_cmp(verbose=True, force="--force" in sys.argv))

@@ -510,3 +510,36 @@ def test_pre_kk_equaliser_parity():
         o = _oracle(gp["stream"], gp["off"], b, cfg, pool, fir, gp["left"], gp["right"], pre_fir=np.float32(g).astype(np.float64))
         rep = _check_buffer(gp, o, b, cfg, pool)
         print("prekk", b, rep)
+
+
+@pytest.mark.parametrize("name,nbuf", [("C2_n16", 3), ("C5", 2)])
+def test_cufft_comparison_x2_parity(name, nbuf):
+    """The cuFFT comparison pipeline (libkkrx_cufft.so, bench.py's `cufft_comparison`
+    leg) computes the same x2 as the method: rel-L2 <= 1e-5 against the oracle's S4 output
+    on every buffer (C5 = the bench workload at full size)."""
+    _require_gpu()
+    import torch
+    from paper_2108_07004_b200 import halo_for
+    from paper_2108_07004_b200.cufft_cmp import CufftS1S4
+    wl = configs.get(name)
+    cfg = wl.link
+    pool = make_pool(cfg, max(nbuf, 2))
+    fir = _fir(name)
+    n = cfg.buffer_len
+    left, right = halo_for(n)
+    stream, off = make_stream(pool, nbuf, left, right)
+    cmp_ = CufftS1S4(n, nbuf, pool.dc_offset, cfg.cspr_db, fir, tone_bin=cfg.tbin)
+    hl, hr = cmp_.halo()
+    assert hl <= left and hr <= right
+    codes = torch.from_numpy(stream).cuda()
+    x2 = torch.empty(nbuf * n // 2, dtype=torch.complex64, device="cuda")
+    cmp_.x2(codes, off, nbuf, x2)
+    torch.cuda.synchronize()
+    x2 = x2.cpu().numpy()
+    for b in range(nbuf):
+        o = _oracle(stream, off, b, cfg, pool, fir, left, right)
+        x2_o = o["x2"][-o["x2_first"]: -o["x2_first"] + n // 2]
+        rel = np.linalg.norm(x2[b * n // 2:(b + 1) * n // 2] - x2_o) / np.linalg.norm(x2_o)
+        print("cufft cmp", name, b, rel)
+        assert rel <= TOL_FIELD, (b, rel)
+    cmp_.close()

@@ -71,3 +71,22 @@ def test_halo_covers_method_needs():
         left, right = halo_for(n, 4096)
         assert left >= O.required_left(4096) and right >= O.required_right()
     assert halo_for(1 << 22, 4096) == (17672, 2312)
+
+
+def test_cufft_comparison_library_exports(root):
+    """libkkrx_cufft.so (the cuFFT comparison pipeline, never the product path) loads,
+    exports what include/kk_cufft_cmp.h declares, and validates its arguments without CUDA."""
+    from paper_2108_07004_b200 import cufft_cmp
+    lib = cufft_cmp.load()
+    txt = open(os.path.join(root, "include", "kk_cufft_cmp.h")).read()
+    names = sorted(set(re.findall(r"^\s*int\s+(kk_cmp_[a-z_0-9]+)\s*\(", txt, re.M)))
+    assert len(names) == 5 and tuple(names) == tuple(sorted(cufft_cmp.EXPORTS))
+    for n in names:
+        assert hasattr(lib, n), n
+    h = C.c_void_p()
+    fir = np.zeros(406, np.float32)
+    fp = fir.ctypes.data_as(C.POINTER(C.c_float))
+    assert lib.kk_cmp_create(C.byref(h), (1 << 16) + 512, 1, 1000.0, 10.0, 1.0, 541065, fp, 203) == -1  # N % 1024
+    assert lib.kk_cmp_create(C.byref(h), 1 << 16, 1, 1000.0, 10.0, 1.0, 541065, fp, 202) == -1         # fir_len
+    assert lib.kk_cmp_create(C.byref(h), 1 << 16, 0, 1000.0, 10.0, 1.0, 541065, fp, 203) == -1         # batch
+    assert lib.kk_cmp_destroy(None) == 0
