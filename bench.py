@@ -436,6 +436,12 @@ def run_gpu(args):
                      "update-pass x2 tails first"),
         "sync_value": samples_total / world / (sync_ms / 1e3) / 1e9 * world,
         "errors": {"bit_errors": int(agg[0]), "bits": int(agg[1]), "ber": int(agg[0]) / max(int(agg[1]), 1)},
+        # context only (north star): the paper's receiver ran the chain in real time at 4 GSa/s
+        # (1 GBaud, 4 sps, 12-bit 4 GS/s ADC) on one commercial GPU "with 5120 processing cores"
+        # that it "almost fully utilizes"; another machine's number
+        "paper_context": {"value": 4.0, "unit": UNIT, "gbaud": 1.0, "hardware": "commercial GPU, 5120 cores",
+                          "cite": "PAPER.md l.25, l.47, l.68, l.167", "ratio": value / world / 4.0,
+                          "note": "per-GPU value / the paper's real-time rate; context, not a baseline"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
