@@ -49,11 +49,57 @@ __host__ __device__ constexpr float cos32(int m) {
 }
 __host__ __device__ constexpr float sin32(int m) { return cos32(m - 8); }
 
+// Complex arithmetic on the packed FP32x2 instructions of sm_100 (FADD2 / FMUL2 / FFMA2:
+// one issue slot for both halves of a float2).  The kernel is instruction-issue bound
+// (DESIGN.md section 6), so this halves the issue cost of the FFT arithmetic.  ptxas
+// folds the operand permutations used below into the instructions' own modifiers:
+// swapped halves (.LO_HI), a per-half sign (.NP), a negated operand and a broadcast scalar
+// or immediate -- checked in the SASS (cuobjdump).  Each half is an IEEE fma /
+// add / mul, identical to the scalar instruction.  -DKK_F32X2=0 restores scalar code.
+#ifndef KK_F32X2
+#define KK_F32X2 1
+#endif
+#if KK_F32X2
+typedef unsigned long long kk_u64;
+__device__ __forceinline__ kk_u64 f2p(float2 a) {
+  kk_u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 p2f(kk_u64 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  kk_u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2p(a)), "l"(f2p(b)));
+  return p2f(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  kk_u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2p(a)), "l"(f2p(b)));
+  return p2f(r);
+}
+// a * b + c per half
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  kk_u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2p(a)), "l"(f2p(b)), "l"(f2p(c)));
+  return p2f(r);
+}
+__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return add2(a, b); }
+__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return add2(a, make_float2(-b.x, -b.y)); }
+// a b = b.x a + b.y (-a.y, a.x): FMUL2 + FFMA2
+__device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
+  return fma2(make_float2(-a.y, a.x), make_float2(b.y, b.y), mul2(a, make_float2(b.x, b.x)));
+}
+#else
 __device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
+#endif
 __device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
 
 // a * exp(-2*pi*i*m/32) (used outside the butterflies)
@@ -65,7 +111,12 @@ __device__ __forceinline__ float2 tw32(float2 a, int m) {
   if (m == 24) return make_float2(-a.y, a.x);
   const float c = cos32(m);
   const float s = -sin32(m);
+#if KK_F32X2
+  // c a + s (-a.y, a.x)
+  return fma2(make_float2(-a.y, a.x), make_float2(s, s), mul2(a, make_float2(c, c)));
+#else
   return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+#endif
 }
 
 // DIT butterfly: (a, b) <- (a + w b, a - w b), w = exp(-2 pi i m / 32), m compile-time.
@@ -88,9 +139,20 @@ __device__ __forceinline__ void bfly(float2& a, float2& b, int m) {
     b = c_sub(a, t);
     a = c_add(a, t);
   } else {
-    // w = c (1 + i t) with c = cos, t = tan (|t| <= tan(3 pi / 8) for the angles used)
     const float c = cos32(m);
     const float s = -sin32(m);
+#if KK_F32X2
+    // w = c (1 + i t), t = s / c (|t| <= tan(7 pi / 16) ~ 5.03; the result's rounding error
+    // stays <= (|c| + |s|) eps |b|): pq = b + t (-b.y, b.x) [one FFMA2 with a swapped,
+    // half-negated operand], then a +- c pq [two FFMA2 with a broadcast immediate]
+    const float t = s / c;
+    const float2 a0 = a;
+    const float2 pq = (m == 4 || m == 12 || m == 20 || m == 28)
+                          ? c_add(b, (t > 0) ? make_float2(-b.y, b.x) : make_float2(b.y, -b.x))
+                          : fma2(make_float2(b.y, b.x), make_float2(-t, t), b);
+    a = fma2(pq, make_float2(c, c), a0);
+    b = fma2(pq, make_float2(-c, -c), a0);
+#else
     if (m == 4 || m == 12 || m == 20 || m == 28) {
       // |t| == 1: p = b.x - t b.y, q = b.y + t b.x are plain adds
       const float t = s / c;
@@ -114,6 +176,7 @@ __device__ __forceinline__ void bfly(float2& a, float2& b, int m) {
       a = make_float2(fmaf(s, p, a0.x), fmaf(s, q, a0.y));
       b = make_float2(fmaf(-s, p, a0.x), fmaf(-s, q, a0.y));
     }
+#endif
   }
 }
 
@@ -217,7 +280,11 @@ __device__ __forceinline__ void fft512_pairs(float2 (&z)[16], int lane, float* _
     float2 other;
     other.x = __shfl_xor_sync(0xffffffffu, mine.x, 1);
     other.y = __shfl_xor_sync(0xffffffffu, mine.y, 1);
+#if KK_F32X2
+    z[r2] = fma2(mine, make_float2(sg, sg), other);
+#else
     z[r2] = make_float2(fmaf(sg, mine.x, other.x), fmaf(sg, mine.y, other.y));
+#endif
   }
 }
 
