@@ -649,8 +649,14 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
         // (kept in shared memory: only phase A reads them)
         const float2* tp = sg.taps + (int64_t)(owner - sg.owner_first) * 8;
         const float2 w = tp[tid], gg = tp[4 + tid];
+#if KK_F32X2
+        // paired: (y.x, y.y) = sum_q P[q] u.x + Q[q] u.y, P = (ta.x, tc.x), Q = (ta.y, tc.y)
+        s_taps[tid] = make_float2(w.x + gg.x, w.y + gg.y);
+        s_taps[4 + tid] = make_float2(gg.y - w.y, w.x - gg.x);
+#else
         s_taps[tid] = make_float2(w.x + gg.x, gg.y - w.y);
         s_taps[4 + tid] = make_float2(w.y + gg.y, w.x - gg.x);
+#endif
       }
     }
     const int16_t* obase = sg.codes + (int64_t)owner * a.N;
@@ -741,8 +747,13 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           for (int j = 0; j < 48; ++j) {
             const int q = PKH + re0 + lane + 32 * j;
             const float vv = fmaxf(prek_v<PREKK>(a, src, q, sg), a.vmin);
-            // 0.5 ln 2 / 1024: the 1/1024 of the inverse FFT is folded in here
+            // 0.5 ln 2 / 1024 (the 1/1024 of the inverse FFT folded in): applied here, or
+            // (KK_F32X2) by the Hilbert mask multiply, the transform being linear
+#if KK_F32X2
+            const float l = lg2_ftz(vv * invd);
+#else
             const float l = lg2_ftz(vv * invd) * (0.34657359027997264f / 1024.0f);
+#endif
             if (j < 32) v[brev(j, 5)].x = l;        // FFT input registers are bit-reversed
             if (j >= 16) v[brev(j - 16, 5)].y = l;
           }
@@ -766,7 +777,13 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
 #pragma unroll
             for (int k2 = 0; k2 < 32; ++k2) {
               const float2 y = v[k2];
+#if KK_F32X2
+              // one FMUL2 per element: swapped halves times -+K, K = 0.5 ln 2 / 1024 (S1 scale)
+              constexpr float KS = 0.34657359027997264f / 1024.0f;
+              float2 r = mul2(make_float2(y.y, y.x), (k2 < 16) ? make_float2(-KS, -KS) : make_float2(KS, KS));
+#else
               float2 r = (k2 < 16) ? make_float2(-y.y, -y.x) : make_float2(y.y, y.x);
+#endif
               if ((k2 == 0 || k2 == 16) && lane == 0) r = make_float2(0.f, 0.f);
               nv[brev(k2, 5)] = r;  // bit-reversed input of the next transform
             }
@@ -806,7 +823,11 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
               const float amp = vv * rsqrt_ftz(vv);
               float sp, cp;
               sincos_small(phi, &sp, &cp);  // |phi| of a few rad at most (KK phase)
+#if KK_F32X2
+              dp0[o] = fma2(make_float2(amp, amp), make_float2(cp, sp), make_float2(-sg.a_hat, 0.f));
+#else
               dp0[o] = make_float2(fmaf(amp, cp, -sg.a_hat), amp * sp);
+#endif
               clip += (cv < a.vmin && (allin || lane + 256 + o < lim)) ? 1u : 0u;
             }
           }
@@ -841,7 +862,11 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           for (int k2 = 0; k2 < 16; ++k2) {
             const float2 s0 = c_mul(v[k2], s_H[lane + 32 * k2]);
             const float2 s1 = c_mul(v[k2 + 16], s_H[lane + 32 * (k2 + 16)]);
+#if KK_F32X2
+            z[brev(k2, 4)] = add2(make_float2(s0.x, -s0.y), make_float2(s1.x, -s1.y));  // conj -> forward DFT = inverse
+#else
             z[brev(k2, 4)] = make_float2(s0.x + s1.x, -(s0.y + s1.y));  // conj -> forward DFT = inverse
+#endif
           }
           fft512_pairs(z, lane, scr, s_tw512);
           const int h = lane & 1, r1 = lane >> 1;
@@ -881,9 +906,15 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           for (int r2 = 0; r2 < 16; ++r2) {
             if (r2 >= lo2 && r2 < hi2) {
               const float2 rr = a.rot[r2];
-              const float ct = fmaf(cb, rr.x, -sb * rr.y), st = fmaf(cb, rr.y, sb * rr.x);
               const float2 o = z[r2];
+#if KK_F32X2
+              // e = e^{i theta_P} = (cb, sb) rr;  conj(o) e = o.x (ct, st) + o.y (st, -ct)
+              const float2 e = c_mul(make_float2(cb, sb), rr);
+              dptr[16 * r2] = fma2(make_float2(e.y, -e.x), make_float2(o.y, o.y), mul2(e, make_float2(o.x, o.x)));
+#else
+              const float ct = fmaf(cb, rr.x, -sb * rr.y), st = fmaf(cb, rr.y, sb * rr.x);
               dptr[16 * r2] = make_float2(o.x * ct + o.y * st, o.x * st - o.y * ct);  // conj(o) e^{i theta}
+#endif
             }
           }
         }
@@ -931,6 +962,17 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
         for (int k = 0; k < SPT; ++k) {
           const int sidx = tid + NWARPS * 32 * k;
           const float2 u[4] = {xs[2 * sidx + 3], xs[2 * sidx + 2], xs[2 * sidx + 1], xs[2 * sidx]};
+#if KK_F32X2
+          // ta = P, tc = Q here (paired taps): two FFMA2 chains, then one FADD2
+          float2 acc0 = mul2(ta[0], make_float2(u[0].x, u[0].x)), acc1 = mul2(ta[1], make_float2(u[1].x, u[1].x));
+          acc0 = fma2(tc[0], make_float2(u[0].y, u[0].y), acc0);
+          acc1 = fma2(tc[1], make_float2(u[1].y, u[1].y), acc1);
+          acc0 = fma2(ta[2], make_float2(u[2].x, u[2].x), acc0);
+          acc1 = fma2(ta[3], make_float2(u[3].x, u[3].x), acc1);
+          acc0 = fma2(tc[2], make_float2(u[2].y, u[2].y), acc0);
+          acc1 = fma2(tc[3], make_float2(u[3].y, u[3].y), acc1);
+          yv[k] = add2(acc0, acc1);
+#else
           float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
 #pragma unroll
           for (int t = 0; t < 4; t += 2) {
@@ -940,6 +982,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
             y1 = fmaf(tc[t + 1].x, u[t + 1].x, fmaf(tc[t + 1].y, u[t + 1].y, y1));
           }
           yv[k] = make_float2(x0 + x1, y0 + y1);
+#endif
         }
       }
       // stage 2: table words (branch-free cell index; uniform table location)
