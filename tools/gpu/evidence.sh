@@ -5,7 +5,7 @@ nvidia-smi > gpurun_out/nvsmi.txt 2>&1
 lscpu > gpurun_out/lscpu.txt 2>&1
 timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_full.log
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
-CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-cufft"
 timeout 300 $CMD > gpurun_out/bench_short.log 2>&1 && \
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "launches rc=$?" >> gpurun_out/ncu_launches.log
