@@ -310,14 +310,21 @@ __device__ __forceinline__ void lms_lanes_body(const LmsArgs& a, unsigned char* 
   }
   for (int i = threadIdx.x; i < 129; i += blockDim.x) s_pts[i] = (i < a.m) ? a.pts[i] : make_float2(INF, INF);
   __syncthreads();
+  // chains spread over the warps (chain blk*blockDim + lane*W + warp): with fewer chains
+  // than threads every warp gets a few lanes, so the rare slow table path of one lane
+  // (divergence) and the per-lane x2 loads cost a warp less; idle lanes replay lane 0's
+  // chain of their warp (same control flow, results dropped); chainless warps leave
+  const int W = (int)(blockDim.x >> 5), wid = (int)(threadIdx.x >> 5), lid = (int)(threadIdx.x & 31);
+  const int c = blk * (int)blockDim.x + lid * W + wid;
+  const int c0 = blk * (int)blockDim.x + wid;
+  if (c0 >= a.nchains) return;
   if (a.wait_ctr) {
-    if ((threadIdx.x & 31) == 0)
+    if (lid == 0)
       while (ld_acquire_u64(a.wait_ctr) < a.wait_target) __nanosleep(200);
     __syncwarp();
   }
-  const int c = blk * blockDim.x + threadIdx.x;
   const bool valid = c < a.nchains;
-  const int cc = valid ? c : a.nchains - 1;  // idle lanes replay the last chain, results dropped
+  const int cc = valid ? c : c0;
   const int b = cc / a.nsub, sblk = cc - b * a.nsub;
   const int64_t n0l = (int64_t)sblk * a.L - a.K;
   const int64_t n0 = (int64_t)b * a.n_sym + n0l;
@@ -1380,8 +1387,7 @@ cudaError_t launch_lms_lanes(const LmsArgs& a, cudaStream_t s) {
     attr_done = true;
   }
   const int ctas = lms_lanes_ctas(a.nchains);
-  const int per = (a.nchains + ctas - 1) / ctas;
-  const int threads = ((per + 31) / 32) * 32;
+  const int threads = LMSL_MAXW * 32;  // chains spread over all warps (lms_lanes_body)
   const int mode = (a.mode == 1) ? 1 : (a.mode == 2 || !(a.inv_tau > 0.f)) ? 2 : 0;
   const size_t sm = LMS_LUT_BYTES + 129 * sizeof(float2);
   if (mode == 1)
