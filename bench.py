@@ -365,7 +365,8 @@ def run_gpu(args):
                 rx.submit_batch(h_stream, off + b0 * N, B, h_out[s & 1])
 
         def e2e_run(packed):
-            submit_host(0, packed)
+            for s in range(args.warmup):  # W untimed steps (every pipeline slot and its staging)
+                submit_host(s, packed)
             rx.sync()
             torch.cuda.synchronize(dev)
             if world > 1:
@@ -468,7 +469,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kk", choices=["kk", "reference"])
     ap.add_argument("--workload", default="C5")
-    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--pool", type=int, default=16)
     ap.add_argument("--ref-workers", type=int, default=0, help="oracle processes (0 = all host cores)")
     ap.add_argument("--no-e2e", action="store_true")

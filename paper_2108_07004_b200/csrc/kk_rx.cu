@@ -1184,8 +1184,14 @@ static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint
     }
   }
   if (a.state != 0) return fail(KK_ESTATE, "async slot busy");
-  kk_status st = slot_reserve(h, a, nbuf, !in_dev, packed);
-  if (st != KK_OK) return st;
+  // grow every slot at once: the pipeline cycles through all NSLOT of them, and device
+  // allocations (cudaMalloc synchronises) must not land in a later, steady-state submit
+  kk_status st = KK_OK;
+  for (int k = 0; k < kk_rx_t::NSLOT; ++k) {
+    if (h->aslot[k].state != 0 && k != s) continue;  // in flight: grows when it is next reused
+    st = slot_reserve(h, h->aslot[k], nbuf, !in_dev, packed);
+    if (st != KK_OK) return st;
+  }
   a.nb = nbuf;
   a.index = h->stream_index;
   a.dc = h->dc;

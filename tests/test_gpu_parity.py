@@ -290,7 +290,7 @@ def test_async_pipeline_equals_process_batch():
 
 
 def test_async_full_size_bench_config():
-    """The bench's launch configuration: C5 (GS-128) at full size, 64-buffer
+    """The bench's launch configuration: C5 (GS-128) at full size, 128-buffer
     submissions through the async pipeline, device-resident.  Two submissions equal
     one process_batch call bit for bit, and one buffer of the batch is checked
     against the float64 oracle."""
@@ -302,7 +302,7 @@ def test_async_full_size_bench_config():
     fir = _fir(name)
     n = cfg.buffer_len
     n_sym = n // 4
-    B = 64
+    B = 128
     left, right = halo_for(n)
     stream, off = make_stream(pool, 2 * B, left, right)
     src = torch.from_numpy(stream).cuda()
@@ -318,8 +318,8 @@ def test_async_full_size_bench_config():
     assert ca == cb
     lab = out_a.cpu().numpy()
     assert np.array_equal(lab, out_b.cpu().numpy())
-    # one buffer (index 37 of the first submission) against the oracle
-    k = 37
+    # one buffer (index 101 of the first submission) against the oracle
+    k = 101
     o = _oracle(stream, off, k, cfg, pool, fir, left, right)
     inv = np.argsort(pool.labels)
     dec = inv[lab[k * n_sym:(k + 1) * n_sym].astype(np.int64)]
