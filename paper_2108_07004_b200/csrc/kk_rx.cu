@@ -51,7 +51,7 @@ struct AsyncSlot {
   const int16_t* codes = nullptr;           // device samples of buffer 0 of the batch
   uint8_t* out_dev = nullptr;               // where the chain writes labels
   uint8_t* out_host = nullptr;              // host destination (D2H after the chain) or NULL
-  cudaEvent_t ev_lms = nullptr, ev_done = nullptr, ev_h2d = nullptr;
+  cudaEvent_t ev_lms = nullptr, ev_done = nullptr, ev_h2d = nullptr, ev_copy = nullptr;
   cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};  // timing: LMS start/end, chain start/end
   bool timed_lms = false, timed_chain = false;
   int state = 0;                            // 0 free, 1 LMS issued + chain deferred, 2 chain issued
@@ -95,7 +95,7 @@ struct kk_rx {
   int a_order[NSLOT] = {-1, -1, -1};       // slots with an issued chain, oldest first
   int a_norder = 0;
   std::vector<kk_rx_counts> a_counts;      // harvested per-buffer counters since the last sync
-  cudaStream_t lms_stream = nullptr, h2d_stream = nullptr;
+  cudaStream_t lms_stream = nullptr, h2d_stream = nullptr, unpack_stream = nullptr;
   cudaEvent_t ev_in = nullptr;
   int64_t a_launches = 0;
   DecLut lut{};
@@ -449,12 +449,13 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
     for (void* q : ap)
       if (q) cudaFree(q);
     if (a.h_counts) cudaFreeHost(a.h_counts);
-    for (cudaEvent_t e : {a.ev_lms, a.ev_done, a.ev_h2d, a.ev_t[0], a.ev_t[1], a.ev_t[2], a.ev_t[3]})
+    for (cudaEvent_t e : {a.ev_lms, a.ev_done, a.ev_h2d, a.ev_copy, a.ev_t[0], a.ev_t[1], a.ev_t[2], a.ev_t[3]})
       if (e) cudaEventDestroy(e);
   }
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->lms_stream) cudaStreamDestroy(h->lms_stream);
   if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
+  if (h->unpack_stream) cudaStreamDestroy(h->unpack_stream);
   for (int i = 0; i < 2; ++i) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_used[i]) cudaEventDestroy(h->ev_used[i]);
@@ -1027,6 +1028,7 @@ static kk_status slot_reserve(kk_rx_t* h, AsyncSlot& a, int64_t nb, bool host_in
     CK(cudaEventCreateWithFlags(&a.ev_lms, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&a.ev_done, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&a.ev_h2d, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&a.ev_copy, cudaEventDisableTiming));
     for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&a.ev_t[k]));
   }
   if (nb > a.cap) {
@@ -1167,6 +1169,7 @@ static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint
   } restore{cur};
   if (!h->h2d_stream) {
     CK(cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->unpack_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
   }
   const bool in_dev = is_device_ptr(first_v);
@@ -1209,9 +1212,13 @@ static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint
     if (in_dev) CK(cudaEventRecord(h->ev_in, h->stream));  // device input: the caller's stream order
     if (in_dev) CK(cudaStreamWaitEvent(h->h2d_stream, h->ev_in, 0));
     CK(cudaMemcpyAsync(a.d_pack, first_b - h->left * 3 / 2, (size_t)(span * 3 / 2), cudaMemcpyDefault, h->h2d_stream));
-    CK(launch_unpack12(a.d_pack, a.d_stage, span, h->h2d_stream));
+    // the unpack runs on its own stream so the next batch's copy follows this one back to
+    // back (the copy engine, not the SMs, is the bound); slot reuse is ordered by ev_done
+    CK(cudaEventRecord(a.ev_copy, h->h2d_stream));
+    CK(cudaStreamWaitEvent(h->unpack_stream, a.ev_copy, 0));
+    CK(launch_unpack12(a.d_pack, a.d_stage, span, h->unpack_stream));
     h->a_launches += 1;
-    CK(cudaEventRecord(a.ev_h2d, h->h2d_stream));
+    CK(cudaEventRecord(a.ev_h2d, h->unpack_stream));
     CK(cudaStreamWaitEvent(h->stream, a.ev_h2d, 0));
     a.codes = a.d_stage + h->left;
   } else if (in_dev) {
