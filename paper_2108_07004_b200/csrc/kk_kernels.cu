@@ -49,6 +49,7 @@ static_assert(LMS_LUT_G * LMS_LUT_G * 8 + 129 * 8 <= SMEM_SHARED + NGROUP * SMEM
 static_assert(WARM2 * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-up codes + tile must fit the x2 window");
 constexpr int WOFF = WARM2 * (int)sizeof(int16_t) / (int)sizeof(float2);  // float2 offset of the warm-up tile in xs
 static_assert(TILE * sizeof(float) <= EQ_KEEP * sizeof(float2), "transpose tile must fit an EQ stride of ebuf");
+static_assert(XS >= 1024 && 3 * 1024 <= STEP, "E-phase 64-bit transpose tiles: three in ebuf[0, STEP), one in xs");
 
 size_t chain_smem_bytes() { return CHAIN_SMEM; }
 
@@ -186,6 +187,12 @@ __device__ __forceinline__ float2 wl_out(const float2 (&w)[4], const float2 (&g)
 }
 
 __device__ __forceinline__ unsigned warp_sum(unsigned v) { return __reduce_add_sync(0xffffffffu, v); }
+
+__device__ __forceinline__ int opaque_i(int x) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
 
 // named barrier of one 4-warp group (ids 1..NGROUP; 0 is __syncthreads)
 __device__ __forceinline__ void group_sync(int gi) {
@@ -530,8 +537,10 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
   float2* s_H = reinterpret_cast<float2*>(smem_raw + SMEM_TW);
   float2* s_tw512 = reinterpret_cast<float2*>(smem_raw + SMEM_TW + SMEM_H);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem_raw + SMEM_TW + SMEM_H + SMEM_TW512);
-  const int gi = threadIdx.x / (NWARPS * 32);      // group of this thread
-  const int tid = threadIdx.x % (NWARPS * 32);     // thread index inside the group
+  // opaque copies: ptxas would otherwise rematerialise these (and the group's smem
+  // pointers) from S2R SR_TID.X at every use under register pressure
+  const int gi = opaque_i(threadIdx.x / (NWARPS * 32));   // group of this thread
+  const int tid = opaque_i(threadIdx.x % (NWARPS * 32));  // thread index inside the group
   unsigned char* gbase = smem_raw + SMEM_SHARED + (size_t)gi * SMEM_GROUP;
   float2* ebuf = reinterpret_cast<float2*>(gbase);
   int16_t* stg = reinterpret_cast<int16_t*>(gbase + SMEM_EBUF);
@@ -770,13 +779,17 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
         }
         // transpose tile: H tasks use their own (not yet written) output slice of ebuf,
         // the warm-up task a slice of xs; E tasks reuse ebuf once every window is loaded.
-        float* scr = wt ? wscr : reinterpret_cast<float*>(ebuf + (isH ? 256 + 1024 * warp : EQ_KEEP * warp));
+        // E tasks: full 32 x 32 float2 tiles (64-bit transposes): warps 0-2 in ebuf[0, 3072)
+        // (the kept tail [3072, 3328) untouched), warp 3 in the x2 window xs, which nothing
+        // reads during phase E and which the epilogue writes only after a group barrier
+        float* scr = wt ? wscr
+                        : reinterpret_cast<float*>(isH ? ebuf + 256 + 1024 * warp : (warp < 3 ? ebuf + 1024 * warp : xs));
         if (!isH) group_sync(gi);  // all E windows are in registers before ebuf becomes scratch
         const int nfft = isH ? 2 : 1;
 #pragma unroll 1
         for (int f = 0; f < nfft; ++f) {
           // H tasks: 64-bit transposes through their own 1024-sample output slice
-          fft1024(v, lane, scr, s_tw, isH && !wt);
+          fft1024(v, lane, scr, s_tw, !wt);
           if (isH && f == 0) {
             // S2: phi = -H{l} <-> +i sgn(k) L_k (reading R1; the /1024 is in S1), conjugated so the
             // next forward FFT computes the inverse: IFFT(Y) = conj(FFT(conj(Y)))
@@ -876,6 +889,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
 #endif
           }
           fft512_pairs(z, lane, scr, s_tw512);
+          group_sync(gi);  // every tile (warp 3's lies in xs) is done before xs is written
           const int h = lane & 1, r1 = lane >> 1;
           // lane holds window outputs rr = r1 + 16 r2 + 256 h, i.e. positions P = P0 + 2 rr: a
           // stride-16 run in x2 index; keep rr in [rlo, 448) and (X2 modes) the owned positions
