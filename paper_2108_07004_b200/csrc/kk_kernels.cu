@@ -50,6 +50,7 @@ static_assert(WARM2 * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-u
 constexpr int WOFF = WARM2 * (int)sizeof(int16_t) / (int)sizeof(float2);  // float2 offset of the warm-up tile in xs
 static_assert(TILE * sizeof(float) <= EQ_KEEP * sizeof(float2), "transpose tile must fit an EQ stride of ebuf");
 static_assert(XS >= 1024 && 3 * 1024 <= STEP, "E-phase 64-bit transpose tiles: three in ebuf[0, STEP), one in xs");
+static_assert(3 * 1024 * sizeof(float) <= SMEM_XS, "pre-KK stash of the three phase-H warps fits the x2 window");
 
 size_t chain_smem_bytes() { return CHAIN_SMEM; }
 
@@ -239,13 +240,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // v = code + d at staged index q, or with the pre-KK intensity equaliser (SURVEY 8(f)
 // NEXT-3) v' = sum_{k=-h..h} g_k code[q - k] + d sum(g) (taps as kernel-parameter operands)
+// int16 -> float without I2F (a quarter-rate XU instruction; the FIR does ~37 per
+// sample): 2^23 + 2^22 + c is exact in fp32 for |c| < 2^22, so one IADD and one exact
+// FADD give (float)c bit for bit
+__device__ __forceinline__ float i16f(int16_t c) { return __int_as_float((int)c + 0x4B400000) - 12582912.0f; }
+
 template <bool PREKK>
 __device__ __forceinline__ float prek_v(const ChainArgs& a, const int16_t* src, int q, const Seg& sg) {
   if (!PREKK) return (float)src[q] + sg.dc;
   float v = sg.prek_dsum;
 #pragma unroll
   for (int k = -PKH; k <= PKH; ++k)
-    if (k >= -a.prek_h && k <= a.prek_h) v = fmaf(a.prek[k + PKH], (float)src[q - k], v);
+    if (k >= -a.prek_h && k <= a.prek_h) v = fmaf(a.prek[k + PKH], i16f(src[q - k]), v);
   return v;
 }
 
@@ -759,10 +765,15 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           // S1: l = 0.5 ln(v/d) (the constant 0.5 ln d is in the DC bin, zeroed by the mask)
           c0 = wt ? 6 * i - 2 : 6 * i + 2 * warp;
           const int re0 = (int)(512 * c0 - 256 - base);
+          // pre-KK FIR: S3 needs v' at exactly this lane's j in [8, 40); keep them (x2 window,
+          // free during phase H except for the warm-up task's tiles in warm steps)
+          float* stash = (PREKK && !warm) ? reinterpret_cast<float*>(xs) + 1024 * warp : nullptr;
 #pragma unroll
           for (int j = 0; j < 48; ++j) {
             const int q = PKH + re0 + lane + 32 * j;
-            const float vv = fmaxf(prek_v<PREKK>(a, src, q, sg), a.vmin);
+            const float cvj = prek_v<PREKK>(a, src, q, sg);
+            if (PREKK && j >= 8 && j < 40 && stash) stash[32 * (j - 8) + lane] = cvj;
+            const float vv = fmaxf(cvj, a.vmin);
             // 0.5 ln 2 / 1024 (the 1/1024 of the inverse FFT folded in): applied here, or
             // (KK_F32X2) by the Hilbert mask multiply, the transform being linear
 #if KK_F32X2
@@ -838,7 +849,9 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
             for (int hh = 0; hh < 2; ++hh) {
               const int o = 32 * t + 512 * hh;
               const float phi = dp0[o].y;
-              const float cv = PREKK ? prek_v<true>(a, sp0, o, sg) : (float)sp0[o] + sg.dc;
+              const float cv = !PREKK ? (float)sp0[o] + sg.dc
+                               : (!warm ? reinterpret_cast<const float*>(xs)[1024 * warp + 32 * (t + 16 * hh) + lane]
+                                        : prek_v<true>(a, sp0, o, sg));
               const float vv = fmaxf(cv, a.vmin);
               const float amp = vv * rsqrt_ftz(vv);
               float sp, cp;

@@ -543,3 +543,52 @@ def test_cufft_comparison_x2_parity(name, nbuf):
         print("cufft cmp", name, b, rel)
         assert rel <= TOL_FIELD, (b, rel)
     cmp_.close()
+
+
+@pytest.mark.parametrize("kind", ["constant", "all_clipped", "nyquist"])
+def test_degenerate_inputs(kind):
+    """Degenerate inputs of the method: constant codes (the intensity of a
+    carrier alone: l constant, so phi = 0 by the zeroed DC bin); codes all below -d (every
+    sample clamped to v_min and counted, outputs finite); a Nyquist-rate square wave (the
+    zeroed Nyquist bin).  GPU E_s vs the oracle at the field tolerance, x2 within 1e-5 of
+    the E_s scale (x2 is the filtered-out tone leakage here), decisions equal outside the
+    exempt set, clip counter exact."""
+    _require_gpu()
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    cfg = configs.get("C1_n16").link
+    pool = make_pool(cfg, 1)
+    fir = _fir("C1_n16")
+    n = cfg.buffer_len
+    left, right = halo_for(n)
+    tot = left + n + right
+    dc = float(np.float32(pool.dc_offset))
+    if kind == "constant":
+        stream = np.full(tot, 37, np.int16)
+    elif kind == "all_clipped":
+        stream = np.full(tot, -2048, np.int16)
+        assert -2048 + dc < 1.0, "dc offset too large for the all-clipped case"
+    else:
+        stream = np.where(np.arange(tot) % 2 == 0, 600, -600).astype(np.int16)
+    rx = KKReceiver(cfg.fmt, n, cfg.cspr_db, fir, dc, tone_bin=cfg.tbin, ref_pattern=pool.pattern,
+                    debug_dump=3, max_batch=1)
+    out = torch.empty(n // 4, dtype=torch.uint8, device="cuda")
+    c = rx.process_batch(torch.from_numpy(stream).cuda(), left, 1, out)[0]
+    o = _oracle(stream, left, 0, cfg, pool, fir, left, right)
+    es_g = rx.debug_es(0, n)
+    es_o = o["e_s"][0 - o["e_pos0"]: n - o["e_pos0"]]
+    assert np.all(np.isfinite(es_g))
+    rel = np.linalg.norm(es_g - es_o) / np.linalg.norm(es_o)
+    assert rel <= TOL_FIELD, rel
+    x2_o = o["x2"]
+    x2_g = rx.debug_x2(o["x2_first"], len(x2_o))
+    assert np.all(np.isfinite(x2_g))
+    assert np.max(np.abs(x2_g - x2_o)) <= 1e-5 * np.max(np.abs(es_o)), (np.max(np.abs(x2_g - x2_o)),)
+    assert c["clipped_samples"] == o["clipped"]
+    if kind == "all_clipped":
+        assert c["clipped_samples"] == n
+    inv = np.argsort(pool.labels)
+    dec_g = inv[out.cpu().numpy().astype(np.int64)]
+    ok = o["margin"] >= EXEMPT
+    assert np.array_equal(dec_g[ok], o["decisions"][ok])
+    print(kind, "es_rel", rel, "exempt", int((~ok).sum()), "clipped", c["clipped_samples"])
+    rx.close()
