@@ -21,7 +21,10 @@ constexpr int STG2 = STG + 2 * PKH;   // staged codes of one step: [3072 i - 256
 constexpr int WARM2 = WARM + 2 * PKH; // staged warm-up codes
 constexpr int XS = 1538;            // x2 window of one step (APPLY): positions 3072 i - 132 + 2 j
 constexpr int NWARPS = 4;          // warps per group
-constexpr int NGROUP = 4;          // independent groups per CTA (one CTA per SM)
+#ifndef KK_NGROUP
+#define KK_NGROUP 4
+#endif
+constexpr int NGROUP = KK_NGROUP;  // independent groups per CTA (one CTA per SM)
 constexpr int TILE = 32 * 33;       // per-warp transpose tile (floats)
 constexpr int SYM_PER_STEP = 768;
 constexpr int MAX_SEG = 4;
