@@ -535,9 +535,11 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (a.lms_ctas > 0 && (int)blockIdx.x >= (int)gridDim.x - a.lms_ctas) {
     // the next batch's LMS update pass: these CTAs come last in the launch order and wait
-    // only for tail steps of this launch, which the chain CTAs never wait for
+    // only for tail steps of this launch, which the chain CTAs never wait for.  Afterwards
+    // they join the chain work (dynamic schedule only) with the shared memory rebuilt
     lms_lanes_body(a.lms, smem_raw, (int)blockIdx.x - ((int)gridDim.x - a.lms_ctas), a.lms_mode);
-    return;
+    if (a.work_ctr == nullptr) return;
+    __syncthreads();
   }
   float2* s_tw = reinterpret_cast<float2*>(smem_raw);
   float2* s_H = reinterpret_cast<float2*>(smem_raw + SMEM_TW);
