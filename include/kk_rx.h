@@ -151,6 +151,9 @@ kk_status kk_rx_process_batch(kk_rx_t *h, const int16_t *first, int64_t nbuf, ui
  * j-1, and that chain launch also computes batch j's update-pass x2 tails.  The
  * chain of the newest batch is launched by the next submit or by kk_rx_sync.
  * Results equal kk_rx_process_batch on the same buffers bit for bit.
+ * Memory: the first submission (and any larger nbuf later) allocates the device staging
+ * of every pipeline slot at once (tails, taps, counters, labels, and for host or packed
+ * input a copy of the batch + halos), so steady-state submits never allocate.
  * `first` (and the halos) must stay valid and unmodified until kk_rx_sync returns;
  * input written by the caller on the handle's cuda_stream before the call is
  * honoured (stream order).  out_symbols: nbuf*buffer_len/4 bytes (device or host)
