@@ -60,3 +60,43 @@ def train_prefir(window, target, d, h, ridge=1e-9):
     AtA = A.T @ A
     AtA += ridge * np.trace(AtA) / (2 * h + 1) * np.eye(2 * h + 1)
     return np.linalg.solve(AtA, A.T @ b)
+
+
+def frame_sync_corr(e_s, e_pos0, points, pattern, n0, n_corr):
+    """Frame synchronisation ("frame-sync correlation against the
+    PCG64 pattern", the step before the FIR fit; the 2^20-symbol PCG64
+    sequence is known to the receiver).  The received field at the symbol instants
+    (4-sps position 4n, reading R15), y_n = E_s[4n], is correlated with the known pattern
+    points over every cyclic lag k of the pattern:
+
+        c(k) = sum_{n=0}^{n_corr-1} y_{n0+n} conj(p[(n0 + n + k) mod P]),  p = points[pattern]
+
+    for all k at once, as a circular cross-correlation by FFT over the pattern period (a
+    library primitive standing for the sum above; tests pin it against the direct sum)."""
+    P = len(pattern)
+    y = e_s[4 * (n0 + np.arange(n_corr, dtype=np.int64)) - e_pos0]
+    q = np.conj(np.asarray(points)[np.asarray(pattern, dtype=np.int64)])
+    ypad = np.zeros(P, dtype=np.complex128)
+    ypad[:n_corr] = y
+    # c'(m) = sum_j y_j q[(j + m) mod P] = IFFT(FFT(q) conj(FFT(conj(y))))(m), m = n0 + k
+    cm = np.fft.ifft(np.fft.fft(q) * np.conj(np.fft.fft(np.conj(ypad))))
+    return np.roll(cm, -n0)  # c[k] = c'(n0 + k)
+
+
+def frame_sync(e_s, e_pos0, points, pattern, n0, n_corr):
+    """The frame offset n_off = argmax_k |c(k)| (lowest k on ties): the symbol sent at
+    buffer index n is pattern[(n + n_off) mod P].  Returns (n_off,
+    c(n_off), mean over k of |c(k)|^2)."""
+    c = frame_sync_corr(e_s, e_pos0, points, pattern, n0, n_corr)
+    mag = np.abs(c) ** 2
+    k = int(np.argmax(mag))
+    return k, c[k], float(np.mean(mag))
+
+
+def frame_sync_direct(e_s, e_pos0, points, pattern, n0, n_corr, k):
+    """c(k) of frame_sync by the plain double sum (the definition), for pins."""
+    P = len(pattern)
+    n = np.arange(n_corr, dtype=np.int64)
+    y = e_s[4 * (n0 + n) - e_pos0]
+    p = np.asarray(points)[np.asarray(pattern, dtype=np.int64)[(n0 + n + k) % P]]
+    return np.sum(y * np.conj(p))

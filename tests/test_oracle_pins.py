@@ -499,3 +499,59 @@ def test_pre_equalizer_lowers_the_bandwidth_error_floor():
     e_eq = evm(s1, p1.dc_offset, g)
     assert e_bw > e_ideal + 3.0          # the roll-off raises the floor
     assert e_eq < e_bw - 3.0             # the pre-KK equaliser removes most of it
+
+
+def test_frame_sync_fft_equals_direct_sum():
+    """oracle.train.frame_sync_corr (FFT form) equals the defining double sum at random
+    lags, including lags whose window wraps the pattern period."""
+    from oracle import train
+    rng = np.random.default_rng(7)
+    P, n0, L = 4096, 37, 300
+    pts = rng.standard_normal(16) + 1j * rng.standard_normal(16)
+    pat = rng.integers(0, 16, P)
+    e_pos0 = -8
+    e_s = rng.standard_normal(4 * (n0 + L) + 16) + 1j * rng.standard_normal(4 * (n0 + L) + 16)
+    c = train.frame_sync_corr(e_s, e_pos0, pts, pat, n0, L)
+    for k in (0, 1, 5, P - L - n0 + 3, P - 1, int(rng.integers(P))):
+        d = train.frame_sync_direct(e_s, e_pos0, pts, pat, n0, L, k)
+        assert abs(c[k] - d) <= 1e-9 * max(1.0, abs(d)), (k, c[k], d)
+
+
+def test_frame_sync_recovers_known_shift():
+    """Symbols of a cyclic pattern sent with a known frame offset s, a fixed phase and AWGN
+    at 10 dB: the correlation peak is at s and stands far above the mean sidelobe."""
+    from oracle import train
+    rng = np.random.default_rng(11)
+    P, s, n0, L = 2048, 1234, 16, 512
+    pts = np.exp(2j * np.pi * np.arange(16) / 16) * (1 + 0.3 * (np.arange(16) % 2))
+    pat = rng.integers(0, 16, P)
+    nsym = n0 + L + 8
+    tx = pts[pat[(np.arange(nsym) + s) % P]] * np.exp(0.7j)
+    tx = tx + 0.3 * (rng.standard_normal(nsym) + 1j * rng.standard_normal(nsym))
+    e_s = np.zeros(4 * nsym, dtype=np.complex128)
+    e_s[0::4] = tx
+    k, ck, mean = train.frame_sync(e_s, 0, pts, pat, n0, L)
+    assert k == s
+    assert abs(ck) ** 2 > 50 * mean
+
+
+def test_frame_sync_on_oracle_field():
+    """End to end on the oracle's S1-S3 field of a synthetic C2 (16-QAM, noisy) buffer read
+    from a point 700 symbols into the stream: frame_sync finds n_off = 700."""
+    from oracle import train
+    from synth import configs
+    from synth.generate import make_pool, make_stream
+    cfg = configs.get("C2_n16").link
+    pool = make_pool(cfg, 2)
+    n = cfg.buffer_len
+    left, right = 2048, 2048
+    st, off = make_stream(pool, 2, left, right)
+    s = 700
+    start = off + 4 * s
+    window = st[start - left: start + n // 2 + right]
+    p = O.RxParams(buffer_len=n, cspr_db=cfg.cspr_db, dc_offset=pool.dc_offset, fir=np.zeros(O.FIR_TAPS),
+                   points=pool.points, labels=pool.labels, tone_bin=cfg.tbin)
+    e_s, e_pos0 = train.field_after_s3(window, left, p)
+    k, ck, mean = train.frame_sync(e_s, e_pos0, pool.points, pool.pattern, 64, 1024)
+    assert k == s
+    assert abs(ck) ** 2 > 20 * mean
