@@ -193,6 +193,19 @@ kk_status kk_rx_set_dc_offset(kk_rx_t *h, float dc_offset);
 kk_status kk_rx_dc_sweep(kk_rx_t *h, const int16_t *first, int64_t nbuf, const float *dc_values, int nd,
                          kk_rx_counts *out_per_dc, int *best);
 
+/* Frame synchronisation (the first init-time step; PAPER l.53,
+ * l.64: the 2^20-symbol PCG64 pattern is known).  Computes E_s of one buffer (same
+ * conventions as kk_rx_process) and correlates its symbol-instant samples
+ * y_n = E_s[4 (n0 + n)], n < n_corr, with the pattern points over every cyclic lag k:
+ *   c(k) = sum_n y_n conj(points[pattern[(n0 + n + k) mod P]]);
+ * *n_off = argmax_k |c(k)| (lowest k on ties): the symbol sent at buffer index n is
+ * pattern[(n + n_off) mod P] -- pass it as ref_offset / to kk_rx_train_fir's symbols.
+ * peak (2 floats, or NULL): c(n_off); peak_to_mean (or NULL): |c(n_off)|^2 / mean_k |c(k)|^2.
+ * Needs ref_pattern; 16 <= n_corr <= 8192; 4*(n0+n_corr-1) < buffer_len.  KK_ESTATE while
+ * the streaming pipeline holds batches. */
+kk_status kk_rx_frame_sync(kk_rx_t *h, const int16_t *buffer, int64_t n0, int32_t n_corr, int64_t *n_off,
+                           float *peak, double *peak_to_mean);
+
 /* Init-time training (the static equaliser "is optimized offline using a
  * training sequence every time that the data acquisition is initialized"; the adaptive
  * equaliser converges "using a training sequence").  All three need an idle streaming

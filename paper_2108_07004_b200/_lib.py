@@ -84,6 +84,8 @@ EXPORTS = {
                                   C.POINTER(C.c_float)]),
     "kk_rx_set_fir": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "kk_rx_train_taps": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_float)]),
+    "kk_rx_frame_sync": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_float), C.POINTER(C.c_double)]),
     "kk_rx_set_w_init": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "kk_rx_dc_sweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_float), C.c_int,
                                  C.POINTER(KKCounts), C.POINTER(C.c_int)]),

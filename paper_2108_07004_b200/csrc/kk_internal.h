@@ -164,6 +164,9 @@ cudaError_t launch_lms(const LmsArgs& a, cudaStream_t s);
 cudaError_t launch_lms_lanes(const LmsArgs& a, cudaStream_t s);
 int lms_lanes_ctas(int nchains);
 cudaError_t launch_apply(const ApplyArgs& a, cudaStream_t s);
+cudaError_t launch_frame_sync(const float2* es, int64_t es_first, int L, const uint8_t* pattern, int64_t P, int64_t n0,
+                              const float2* pts, int m, unsigned long long* best, double* sum2, float2* cval,
+                              cudaStream_t s);
 cudaError_t launch_train_fir(const float2* es, int64_t pos_first, const float2* sym, int n_count, int ntap, double ridge,
                              double2* R, double2* b, float* out, cudaStream_t s);
 cudaError_t launch_gmi(const float2* pts, const uint8_t* labs, int m, int nb, const double2* nodes, const double* wts,

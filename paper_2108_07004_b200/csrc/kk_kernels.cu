@@ -1581,6 +1581,66 @@ __global__ void __launch_bounds__(256) kk_chol_solve_kernel(double2* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Frame synchronisation (oracle.train.frame_sync): correlation
+// of the symbol-instant field y_n = E_s[4 (n0 + n)], n < L, with the known pattern
+// points over every cyclic lag k of the pattern,
+//   c(k) = sum_n y_n conj(p[(n0 + n + k) mod P]),   n_off = argmax_k |c(k)| (lowest k on ties).
+// One thread per lag; y and the points in shared memory, pattern bytes coalesced across
+// lags; per-warp max of (|c|^2, k) -> one 64-bit atomicMax per warp (|c|^2 bits in the
+// high word -- order-preserving for non-negative floats -- and ~k in the low word so
+// equal magnitudes keep the lowest k); sum of |c|^2 for the mean sidelobe level.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) kk_fsync_kernel(const float2* __restrict__ es, int64_t es_first, int L,
+                                                       const uint8_t* __restrict__ pattern, int64_t P, int64_t n0,
+                                                       const float2* __restrict__ pts, int m,
+                                                       unsigned long long* __restrict__ best, double* __restrict__ sum2,
+                                                       float2* __restrict__ cval) {
+  extern __shared__ float2 fs_y[];  // L field samples, then the points
+  float2* fs_p = fs_y + L;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) fs_y[i] = es[es_first + 4 * (int64_t)i];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) fs_p[i] = pts[i];
+  __syncthreads();
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float cr = 0.f, ci = 0.f;
+  if (k < P) {
+    int64_t idx = (n0 + k) % P;
+    for (int n = 0; n < L; ++n) {
+      const float2 y = fs_y[n], p = fs_p[pattern[idx]];
+      cr = fmaf(y.x, p.x, fmaf(y.y, p.y, cr));  // y conj(p)
+      ci = fmaf(y.y, p.x, fmaf(-y.x, p.y, ci));
+      idx = (idx + 1 == P) ? 0 : idx + 1;
+    }
+    if (cval) cval[k] = make_float2(cr, ci);
+  }
+  const float mag = (k < P) ? fmaf(cr, cr, ci * ci) : 0.f;
+  unsigned long long key = (k < P) ? (((unsigned long long)__float_as_uint(mag) << 32) | (unsigned)(~(unsigned)k)) : 0ull;
+  double sm = (double)mag;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
+    key = ok > key ? ok : key;
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(best, key);
+    atomicAdd(sum2, sm);
+  }
+}
+
+cudaError_t launch_frame_sync(const float2* es, int64_t es_first, int L, const uint8_t* pattern, int64_t P, int64_t n0,
+                              const float2* pts, int m, unsigned long long* best, double* sum2, float2* cval,
+                              cudaStream_t s) {
+  const size_t sm = (size_t)(L + m) * sizeof(float2);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kk_fsync_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t blocks = (P + 255) / 256;
+  kk_fsync_kernel<<<(unsigned)blocks, 256, sm, s>>>(es, es_first, L, pattern, P, n0, pts, m, best, sum2, cval);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_train_fir(const float2* es, int64_t pos_first, const float2* sym, int n_count, int ntap, double ridge,
                              double2* R, double2* b, float* out, cudaStream_t s) {
   const int nt = (ntap + GRAM_T - 1) / GRAM_T;

@@ -1473,6 +1473,68 @@ extern "C" kk_status kk_rx_train_fir(kk_rx_t* h, const int16_t* buffer, const fl
   return st;
 }
 
+// SURVEY 8(f) NEXT row 2, first step of the init-time training: frame synchronisation
+// against the known PCG64 pattern (oracle.train.frame_sync).  E_s of one buffer by the
+// chain kernel, then kk_fsync_kernel over every cyclic lag of the pattern.
+extern "C" kk_status kk_rx_frame_sync(kk_rx_t* h, const int16_t* buffer, int64_t n0, int32_t n_corr, int64_t* n_off,
+                                      float* peak, double* peak_to_mean) {
+  if (!h || !buffer || !n_off) return fail(KK_EINVAL, "bad arguments");
+  if (!h->has_pattern) return fail(KK_EINVAL, "frame synchronisation needs ref_pattern");
+  if (n_corr < 16 || n_corr > 8192 || n0 < 0 || 4 * (n0 + (int64_t)n_corr - 1) >= h->N)
+    return fail(KK_EINVAL, "need 16 <= n_corr <= 8192, n0 >= 0 and 4*(n0+n_corr-1) < buffer_len");
+  if (!pipeline_idle(h)) return fail(KK_ESTATE, "kk_rx_sync the streaming pipeline first");
+  CK(cudaSetDevice(h->device));
+  int16_t* tmp = nullptr;
+  const int16_t* dev0 = nullptr;
+  kk_status st = stage_one(h, buffer, &tmp, &dev0);
+  if (st != KK_OK) return st;
+  float2 *x2 = nullptr, *es = nullptr, *cval = nullptr;
+  unsigned long long* best = nullptr;
+  double* sum2 = nullptr;
+  auto release = [&]() {
+    void* ptrs[] = {tmp, x2, es, cval, best, sum2};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+  };
+  cudaError_t e = cudaMalloc(&x2, (size_t)(h->x2h + h->N / 2 + 64) * sizeof(float2));
+  if (e == cudaSuccess) e = cudaMalloc(&es, (size_t)h->N * sizeof(float2));
+  if (e == cudaSuccess && peak) e = cudaMalloc(&cval, (size_t)h->P * sizeof(float2));
+  if (e == cudaSuccess) e = cudaMalloc(&best, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&sum2, sizeof(double));
+  if (e == cudaSuccess) e = cudaMemsetAsync(best, 0, sizeof(unsigned long long), h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(sum2, 0, sizeof(double), h->stream);
+  if (e != cudaSuccess) {
+    release();
+    return fail(KK_ENOMEM, std::string("kk_rx_frame_sync: ") + cudaGetErrorString(e));
+  }
+  st = one_buffer_stages(h, dev0, x2, es);
+  if (st == KK_OK) {
+    unsigned long long hb = 0;
+    double hs = 0.0;
+    float2 hc = make_float2(0.f, 0.f);
+    e = launch_frame_sync(es, 4 * n0, n_corr, h->d_pattern, h->P, n0, h->d_pts, h->m, best, sum2, cval, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hb, best, sizeof(hb), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hs, sum2, sizeof(hs), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    const int64_t k = (int64_t)(uint32_t)~(uint32_t)(hb & 0xffffffffull);
+    if (e == cudaSuccess && peak) e = cudaMemcpy(&hc, cval + k, sizeof(hc), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      h->sticky = KK_ECUDA;
+      st = fail(KK_ECUDA, std::string("kk_rx_frame_sync: ") + cudaGetErrorString(e));
+    } else {
+      *n_off = k;
+      if (peak) {
+        peak[0] = hc.x;
+        peak[1] = hc.y;
+      }
+      const double mag = (double)__builtin_bit_cast(float, (uint32_t)(hb >> 32));
+      if (peak_to_mean) *peak_to_mean = (hs > 0.0) ? mag / (hs / (double)h->P) : 0.0;
+    }
+  }
+  release();
+  return st;
+}
+
 extern "C" kk_status kk_rx_set_fir(kk_rx_t* h, const float* fir) {
   if (!h || !fir) return fail(KK_EINVAL, "bad arguments");
   if (!pipeline_idle(h)) return fail(KK_ESTATE, "kk_rx_sync the streaming pipeline first");

@@ -191,6 +191,18 @@ class KKReceiver:
         c = out[0::2] + 1j * out[1::2].astype(np.float64)
         return c[:4], c[4:]
 
+    def frame_sync(self, stream, offset, n0=64, n_corr=2048):
+        """kk_rx_frame_sync: (n_off, c(n_off) complex, peak-to-mean ratio) of the buffer at
+        `offset`: the symbol sent at buffer index n is pattern[(n + n_off) mod P]."""
+        base, es = _ptr(stream)
+        assert es == 2
+        k = C.c_int64()
+        pk = np.zeros(2, dtype=np.float32)
+        ratio = C.c_double()
+        check(self._lib.kk_rx_frame_sync(self.h, C.c_void_p(base + 2 * int(offset)), int(n0), int(n_corr), C.byref(k),
+                                          _fptr(pk), C.byref(ratio)), "kk_rx_frame_sync")
+        return int(k.value), complex(pk[0], pk[1]), float(ratio.value)
+
     def set_w_init(self, w, g):
         c = np.r_[np.asarray(w, dtype=np.complex128), np.asarray(g, dtype=np.complex128)]
         ff = np.ascontiguousarray(np.stack([c.real, c.imag], -1).reshape(-1).astype(np.float32))

@@ -5,8 +5,8 @@ tests/test_gpu_parity.py; this is the measurement half of the bar).  C5 workload
     python tools/next_rows_bench.py [B] > profiles/.../next_rows.json
 
   row 1  DC-offset sweep (kk_rx_dc_sweep): 5 hypotheses over B buffers
-  row 2  init-time training: kk_rx_train_fir (LS 203 taps from 8192 symbols) and
-         kk_rx_train_taps (4096 PILOT LMS steps)
+  row 2  init-time training: kk_rx_frame_sync (all 2^20 lags), kk_rx_train_fir (LS 203
+         taps from 8192 symbols) and kk_rx_train_taps (4096 PILOT LMS steps)
   row 3  pre-KK intensity equaliser: streaming throughput with a 15-tap pre-FIR vs without
   row 4  GMI of constellations (kk_gmi_awgn): batched evaluations per second
 """
@@ -100,8 +100,13 @@ def wall(fn, reps=3):
 t_fir = wall(lambda: rx2.train_fir(src_t, off_t, sym[32:32 + 8192], 32))
 rx2.set_fir(fir)
 t_taps = wall(lambda: rx2.train_taps(src_t, off_t, 4096))
+t_fs = wall(lambda: rx2.frame_sync(src_t, off_t, 64, 2048))
+fs = rx2.frame_sync(src_t, off_t, 64, 2048)
 res["row2_training"] = {"train_fir_ms": t_fir, "train_fir": "LS 203-tap FIR from 8192 training symbols (fp64 Gram + Cholesky on the GPU), host wall time incl. the copy-back",
-                        "train_taps_ms": t_taps, "train_taps": "4096 PILOT LMS steps from W_init, host wall time"}
+                        "train_taps_ms": t_taps, "train_taps": "4096 PILOT LMS steps from W_init, host wall time",
+                        "frame_sync_ms": t_fs, "frame_sync": "all 2^20 cyclic lags x 2048 symbol-instant samples "
+                        "(E_s of one buffer + kk_fsync_kernel), host wall time",
+                        "frame_sync_result": {"n_off": fs[0], "peak_to_mean": fs[2]}}
 rx2.close()
 # row 4: GMI evaluations per second (GS-128 at 20 dB, Gauss-Hermite order 6, batches of 256 label permutations)
 pts, labs = load_constellation("GS128")
