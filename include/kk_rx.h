@@ -193,6 +193,19 @@ kk_status kk_rx_set_dc_offset(kk_rx_t *h, float dc_offset);
 kk_status kk_rx_dc_sweep(kk_rx_t *h, const int16_t *first, int64_t nbuf, const float *dc_values, int nd,
                          kk_rx_counts *out_per_dc, int *best);
 
+/* Generalised sweep ("batched DC-offset (and CSPR-hypothesis)
+ * sweep"): hypothesis k uses DC offset dc_values[k] and, when cspr_db_values != NULL,
+ * CSPR cspr_db_values[k] (A_hat = sqrt(d c/(1+c)), c = 10^(CSPR/10), reading R6); NULL
+ * keeps the handle's CSPR (= kk_rx_dc_sweep).  Same outputs and conventions as
+ * kk_rx_dc_sweep; the handle's offset and CSPR are restored afterwards.
+ * KK_EINVAL: dc <= 0, |CSPR| >= 60 dB, nd <= 0, nbuf <= 0. */
+kk_status kk_rx_sweep(kk_rx_t *h, const int16_t *first, int64_t nbuf, const float *dc_values,
+                      const float *cspr_db_values, int nd, kk_rx_counts *out_per_hyp, int *best);
+
+/* Set the CSPR hypothesis (dB) of the handle: A_hat = sqrt(d c/(1+c)) with the current DC
+ * offset.  Takes effect for batches submitted afterwards.  KK_EINVAL if |CSPR| >= 60 dB. */
+kk_status kk_rx_set_cspr(kk_rx_t *h, float cspr_db);
+
 /* Frame synchronisation (the first init-time step; PAPER l.53,
  * l.64: the 2^20-symbol PCG64 pattern is known).  Computes E_s of one buffer (same
  * conventions as kk_rx_process) and correlates its symbol-instant samples

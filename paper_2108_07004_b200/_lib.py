@@ -89,6 +89,9 @@ EXPORTS = {
     "kk_rx_set_w_init": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "kk_rx_dc_sweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_float), C.c_int,
                                  C.POINTER(KKCounts), C.POINTER(C.c_int)]),
+    "kk_rx_sweep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_int,
+                              C.POINTER(KKCounts), C.POINTER(C.c_int)]),
+    "kk_rx_set_cspr": (C.c_int, [C.c_void_p, C.c_float]),
     "kk_rx_get_taps": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_float)]),
     "kk_rx_totals": (C.c_int, [C.c_void_p, C.POINTER(KKCounts)]),
     "kk_rx_reset_totals": (C.c_int, [C.c_void_p]),

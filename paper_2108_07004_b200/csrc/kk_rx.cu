@@ -1338,16 +1338,33 @@ extern "C" kk_status kk_rx_set_dc_offset(kk_rx_t* h, float dc_offset) {
 // "all measurements are performed multiple times using different DC offset
 // values" and the best Q is kept.  Each hypothesis is a full S1-S7 pass over the same
 // buffers; the hypotheses run back to back through the streaming pipeline.
-extern "C" kk_status kk_rx_dc_sweep(kk_rx_t* h, const int16_t* first, int64_t nbuf, const float* dc_values, int nd,
-                                    kk_rx_counts* out_per_dc, int* best) {
+extern "C" kk_status kk_rx_set_cspr(kk_rx_t* h, float cspr_db) {
+  if (!h) return fail(KK_EINVAL, "null handle");
+  if (!(cspr_db > -60.f && cspr_db < 60.f)) return fail(KK_EINVAL, "cspr_db out of range");
+  h->cspr_lin = std::pow(10.0, (double)cspr_db / 10.0);
+  h->a_hat = (float)std::sqrt((double)h->dc * h->cspr_lin / (1.0 + h->cspr_lin));  // reading R6
+  return KK_OK;
+}
+
+// "batched DC-offset (and CSPR-hypothesis) sweep".  Hypothesis k
+// runs S1-S7 over the same buffers with DC offset dc_values[k] and, if cspr_db_values is
+// given, CSPR cspr_db_values[k] (A_hat = sqrt(d c / (1 + c)), reading R6); the hypotheses go
+// back to back through the streaming pipeline (each slot carries its own d and A_hat).
+extern "C" kk_status kk_rx_sweep(kk_rx_t* h, const int16_t* first, int64_t nbuf, const float* dc_values,
+                                 const float* cspr_db_values, int nd, kk_rx_counts* out_per_hyp, int* best) {
   if (!h || !first || !dc_values || nd <= 0 || nbuf <= 0) return fail(KK_EINVAL, "bad arguments");
-  for (int k = 0; k < nd; ++k)
+  for (int k = 0; k < nd; ++k) {
     if (!(dc_values[k] > 0.f)) return fail(KK_EINVAL, "dc_values must be > 0");
+    if (cspr_db_values && !(cspr_db_values[k] > -60.f && cspr_db_values[k] < 60.f))
+      return fail(KK_EINVAL, "cspr_db_values out of range");
+  }
   const float dc0 = h->dc;
+  const double c0 = h->cspr_lin;
   const int64_t idx0 = h->stream_index;
   kk_status st = kk_rx_sync(h, nullptr, 0, nullptr);  // start from an empty pipeline
   if (st != KK_OK) return st;
   for (int k = 0; k < nd; ++k) {
+    if (cspr_db_values) h->cspr_lin = std::pow(10.0, (double)cspr_db_values[k] / 10.0);
     kk_rx_set_dc_offset(h, dc_values[k]);
     h->stream_index = idx0;
     st = kk_rx_submit_batch(h, first, nbuf, nullptr);
@@ -1356,10 +1373,11 @@ extern "C" kk_status kk_rx_dc_sweep(kk_rx_t* h, const int16_t* first, int64_t nb
   std::vector<kk_rx_counts> per((size_t)nd * nbuf);
   int64_t n = 0;
   if (st == KK_OK) st = kk_rx_sync(h, per.data(), (int64_t)per.size(), &n);
+  h->cspr_lin = c0;
   kk_rx_set_dc_offset(h, dc0);
   h->stream_index = idx0 + nbuf;
   if (st != KK_OK) return st;
-  if (n != (int64_t)nd * nbuf) return fail(KK_ECUDA, "dc sweep: unexpected result count");
+  if (n != (int64_t)nd * nbuf) return fail(KK_ECUDA, "sweep: unexpected result count");
   int kb = 0;
   double ber_b = 2.0;
   for (int k = 0; k < nd; ++k) {
@@ -1374,7 +1392,7 @@ extern "C" kk_status kk_rx_dc_sweep(kk_rx_t* h, const int16_t* first, int64_t nb
       t.gated_updates += c.gated_updates;
       t.flags |= c.flags;
     }
-    if (out_per_dc) out_per_dc[k] = t;
+    if (out_per_hyp) out_per_hyp[k] = t;
     const double ber = t.bits ? (double)t.bit_errors / (double)t.bits : 0.0;
     if (ber < ber_b) {
       ber_b = ber;
@@ -1383,6 +1401,11 @@ extern "C" kk_status kk_rx_dc_sweep(kk_rx_t* h, const int16_t* first, int64_t nb
   }
   if (best) *best = kb;
   return KK_OK;
+}
+
+extern "C" kk_status kk_rx_dc_sweep(kk_rx_t* h, const int16_t* first, int64_t nbuf, const float* dc_values, int nd,
+                                    kk_rx_counts* out_per_dc, int* best) {
+  return kk_rx_sweep(h, first, nbuf, dc_values, nullptr, nd, out_per_dc, best);
 }
 
 

@@ -164,6 +164,24 @@ class KKReceiver:
                                        cnt, C.byref(best)), "kk_rx_dc_sweep")
         return [c.as_dict() for c in cnt], int(best.value)
 
+    def set_cspr(self, cspr_db):
+        check(self._lib.kk_rx_set_cspr(self.h, float(cspr_db)), "kk_rx_set_cspr")
+
+    def sweep(self, stream, offset, nbuf, dc_values, cspr_db_values=None):
+        """kk_rx_sweep: counters (summed over the nbuf buffers) per (DC offset, CSPR)
+        hypothesis and the index of the best (lowest BER) one."""
+        base, es = _ptr(stream)
+        assert es == 2
+        dv = np.ascontiguousarray(np.asarray(dc_values, dtype=np.float32))
+        cv = None if cspr_db_values is None else np.ascontiguousarray(np.asarray(cspr_db_values, dtype=np.float32))
+        assert cv is None or len(cv) == len(dv)
+        cnt = (KKCounts * len(dv))()
+        best = C.c_int()
+        check(self._lib.kk_rx_sweep(self.h, C.c_void_p(base + 2 * int(offset)), int(nbuf), _fptr(dv),
+                                    _fptr(cv) if cv is not None else None, len(dv), cnt, C.byref(best)),
+              "kk_rx_sweep")
+        return [c.as_dict() for c in cnt], int(best.value)
+
     def train_fir(self, stream, offset, symbols, n_first, ridge=1e-9):
         """kk_rx_train_fir: LS 203-tap static equaliser from the buffer at `offset` whose
         transmitted symbols n_first .. n_first+len(symbols)-1 are `symbols` (complex)."""

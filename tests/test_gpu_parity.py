@@ -623,3 +623,50 @@ def test_frame_sync_matches_oracle(name, shift):
     assert abs(c_g - c_o) <= 1e-4 * abs(c_o)
     assert ratio > 100
     rx.close()
+
+
+def test_cspr_hypothesis_sweep():
+    """NEXT row 1, CSPR-hypothesis part: kk_rx_sweep over (d, CSPR) pairs.
+    The nominal pair equals a plain call bit for bit; an off-nominal CSPR hypothesis meets
+    the oracle parity contract with the oracle run at that CSPR (A_hat, reading R6); the
+    handle's CSPR is restored afterwards."""
+    _require_gpu()
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    name = "C2_n16"
+    cfg = configs.get(name).link
+    pool = make_pool(cfg, 2)
+    fir = _fir(name)
+    n = cfg.buffer_len
+    left, right = halo_for(n)
+    stream, off = make_stream(pool, 2, left, right)
+    src = torch.from_numpy(stream).cuda()
+    d0 = float(pool.dc_offset)
+    cs = [cfg.cspr_db - 3.0, cfg.cspr_db, cfg.cspr_db + 3.0]
+    rx = KKReceiver(cfg.fmt, n, cfg.cspr_db, fir, d0, tone_bin=cfg.tbin, ref_pattern=pool.pattern)
+    per, best = rx.sweep(src, off, 2, [d0] * 3, cs)
+    ref = KKReceiver(cfg.fmt, n, cfg.cspr_db, fir, d0, tone_bin=cfg.tbin, ref_pattern=pool.pattern)
+    c = ref.process_batch(src, off, 2)
+    assert per[1]["bit_errors"] == sum(x["bit_errors"] for x in c)
+    assert per[1]["sym_errors"] == sum(x["sym_errors"] for x in c)
+    c_again = rx.process_batch(src, off, 2)  # CSPR restored
+    assert [x["bit_errors"] for x in c_again] == [x["bit_errors"] for x in c]
+    # the +3 dB hypothesis through the oracle
+    rx1 = KKReceiver(cfg.fmt, n, cs[2], fir, d0, tone_bin=cfg.tbin, ref_pattern=pool.pattern, debug_dump=3,
+                     max_batch=2)
+    out = torch.empty(2 * (n // 4), dtype=torch.uint8, device="cuda")
+    c1 = rx1.process_batch(src, off, 2, out)
+    assert per[2]["bit_errors"] == sum(x["bit_errors"] for x in c1)
+    win = stream[off - left: off + n + right]
+    p = O.RxParams(buffer_len=n, cspr_db=cs[2], dc_offset=np.float32(d0), fir=fir, points=pool.points,
+                   labels=pool.labels, tone_bin=cfg.tbin, pattern=pool.pattern)
+    o = O.receive(win, left, p, want_stages=True)
+    x2_g = rx1.debug_x2(o["x2_first"], len(o["x2"]))
+    assert np.linalg.norm(x2_g - o["x2"]) / np.linalg.norm(o["x2"]) <= TOL_FIELD
+    inv = np.argsort(pool.labels)
+    dec_g = inv[out.cpu().numpy()[: n // 4].astype(np.int64)]
+    ok = o["margin"] >= EXEMPT
+    assert np.all(dec_g[ok] == o["decisions"][ok])
+    print("cspr sweep BER", [x["bit_errors"] / x["bits"] for x in per], "best", best)
+    rx.close()
+    ref.close()
+    rx1.close()
