@@ -51,7 +51,8 @@ struct AsyncSlot {
   const int16_t* codes = nullptr;           // device samples of buffer 0 of the batch
   uint8_t* out_dev = nullptr;               // where the chain writes labels
   uint8_t* out_host = nullptr;              // host destination (D2H after the chain) or NULL
-  cudaEvent_t ev_lms = nullptr, ev_done = nullptr, ev_h2d = nullptr, ev_copy = nullptr;
+  cudaEvent_t ev_lms = nullptr, ev_done = nullptr, ev_h2d = nullptr, ev_copy = nullptr, ev_zero = nullptr,
+              ev_chain = nullptr;
   cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};  // timing: LMS start/end, chain start/end
   bool timed_lms = false, timed_chain = false;
   int state = 0;                            // 0 free, 1 LMS issued + chain deferred, 2 chain issued
@@ -85,17 +86,21 @@ struct kk_rx {
   // and the monotone tail-step counter of the async pipeline
   unsigned long long* d_ctr = nullptr;
   int ctr_next = 0;
+  static constexpr int CTR_POOL = 4096;  // dynamic-schedule work counters (use_dyn)
   unsigned long long tail_done_target = 0;
   bool dyn_sched = true;
   unsigned long long* d_dbg = nullptr;     // KKRX_PHASE_TIMING diagnostics
   // asynchronous pipeline
-  static constexpr int NSLOT = 3;         // batches in flight: LMS(j) | chain(j-1) queued | chain(j-2) running
+#ifndef KK_NSLOT
+#define KK_NSLOT 3
+#endif
+  static constexpr int NSLOT = KK_NSLOT;  // batches in flight: LMS(j) | chain(j-1) queued | chain(j-2) running
   AsyncSlot aslot[NSLOT];
   int a_next = 0, a_deferred = -1;
-  int a_order[NSLOT] = {-1, -1, -1};       // slots with an issued chain, oldest first
+  int a_order[NSLOT] = {};       // slots with an issued chain, oldest first
   int a_norder = 0;
   std::vector<kk_rx_counts> a_counts;      // harvested per-buffer counters since the last sync
-  cudaStream_t lms_stream = nullptr, h2d_stream = nullptr, unpack_stream = nullptr;
+  cudaStream_t lms_stream = nullptr, h2d_stream = nullptr, unpack_stream = nullptr, aux_stream = nullptr;
   cudaEvent_t ev_in = nullptr;
   int64_t a_launches = 0;
   DecLut lut{};
@@ -425,6 +430,8 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
   cudaGetDevice(&cur);
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  for (cudaStream_t q : {h->aux_stream, h->unpack_stream, h->h2d_stream})
+    if (q) cudaStreamSynchronize(q);
   if (h->d_dbg) {
     unsigned long long t[8] = {0};
     cudaMemcpy(t, h->d_dbg, sizeof(t), cudaMemcpyDeviceToHost);
@@ -449,13 +456,15 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
     for (void* q : ap)
       if (q) cudaFree(q);
     if (a.h_counts) cudaFreeHost(a.h_counts);
-    for (cudaEvent_t e : {a.ev_lms, a.ev_done, a.ev_h2d, a.ev_copy, a.ev_t[0], a.ev_t[1], a.ev_t[2], a.ev_t[3]})
+    for (cudaEvent_t e : {a.ev_lms, a.ev_done, a.ev_h2d, a.ev_copy, a.ev_zero, a.ev_chain, a.ev_t[0], a.ev_t[1],
+                          a.ev_t[2], a.ev_t[3]})
       if (e) cudaEventDestroy(e);
   }
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->lms_stream) cudaStreamDestroy(h->lms_stream);
   if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
   if (h->unpack_stream) cudaStreamDestroy(h->unpack_stream);
+  if (h->aux_stream) cudaStreamDestroy(h->aux_stream);
   for (int i = 0; i < 2; ++i) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_used[i]) cudaEventDestroy(h->ev_used[i]);
@@ -680,8 +689,8 @@ kk_status kk_rx_create(kk_rx_t** out, int fmt, int sps, int64_t buffer_len, floa
   }
   CKC(chain_setup(dev, &h->grid_chain));
   CKC(lms_setup());
-  CKC(cudaMalloc(&h->d_ctr, 64 * sizeof(unsigned long long)));
-  CKC(cudaMemset(h->d_ctr, 0, 64 * sizeof(unsigned long long)));
+  CKC(cudaMalloc(&h->d_ctr, (8 + kk_rx_t::CTR_POOL) * sizeof(unsigned long long)));
+  CKC(cudaMemset(h->d_ctr, 0, (8 + kk_rx_t::CTR_POOL) * sizeof(unsigned long long)));
   if (const char* e = std::getenv("KKRX_STATIC_SCHED")) h->dyn_sched = (e[0] == '0');
   if (const char* e = std::getenv("KKRX_PHASE_TIMING")) {
     if (e[0] == '1') {
@@ -764,9 +773,17 @@ static cudaError_t use_dyn(kk_rx_t* h, ChainArgs& ca, cudaStream_t st) {
     ca.work_ctr = nullptr;
     return cudaSuccess;
   }
-  unsigned long long* c = h->d_ctr + 8 + (h->ctr_next++ % 32);
-  ca.work_ctr = c;
-  return cudaMemsetAsync(c, 0, sizeof(unsigned long long), st);
+  // a fresh counter from a pool zeroed ahead of use: each half is re-zeroed (one memset)
+  // when the other half starts, CTR_POOL/2 launches after its own last use -- far beyond
+  // the launches in flight -- so no per-launch memset sits between chain launches
+  const int slot = h->ctr_next++ % kk_rx_t::CTR_POOL;
+  if (slot % (kk_rx_t::CTR_POOL / 2) == 0 && h->ctr_next > kk_rx_t::CTR_POOL / 2) {
+    const int other = (slot + kk_rx_t::CTR_POOL / 2) % kk_rx_t::CTR_POOL;
+    cudaError_t e = cudaMemsetAsync(h->d_ctr + 8 + other, 0, (kk_rx_t::CTR_POOL / 2) * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+  }
+  ca.work_ctr = h->d_ctr + 8 + slot;
+  return cudaSuccess;
 }
 
 static kk_status grow(kk_rx_t* h, int64_t nb) {
@@ -1029,6 +1046,8 @@ static kk_status slot_reserve(kk_rx_t* h, AsyncSlot& a, int64_t nb, bool host_in
     CK(cudaEventCreateWithFlags(&a.ev_done, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&a.ev_h2d, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&a.ev_copy, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&a.ev_zero, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&a.ev_chain, cudaEventDisableTiming));
     for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&a.ev_t[k]));
   }
   if (nb > a.cap) {
@@ -1138,11 +1157,14 @@ static kk_status issue_chain(kk_rx_t* h, int p, int t, const LmsArgs* la) {
   if (h->timing) CK(cudaEventRecord(ap.ev_t[3], h->stream));
   ap.timed_chain = h->timing;
   h->a_launches += 1;
+  // results back to the host on the auxiliary stream, behind the chain
+  CK(cudaEventRecord(ap.ev_chain, h->stream));
+  CK(cudaStreamWaitEvent(h->aux_stream, ap.ev_chain, 0));
   if (ap.out_host)
-    CK(cudaMemcpyAsync(ap.out_host, ap.out_dev, (size_t)ap.nb * h->n_sym, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(ap.out_host, ap.out_dev, (size_t)ap.nb * h->n_sym, cudaMemcpyDeviceToHost, h->aux_stream));
   CK(cudaMemcpyAsync(ap.h_counts, ap.d_counts, (size_t)ap.nb * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                     h->stream));
-  CK(cudaEventRecord(ap.ev_done, h->stream));
+                     h->aux_stream));
+  CK(cudaEventRecord(ap.ev_done, h->aux_stream));
   ap.state = 2;
   h->a_order[h->a_norder++] = p;
   return KK_OK;
@@ -1170,6 +1192,7 @@ static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint
   if (!h->h2d_stream) {
     CK(cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&h->unpack_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
   }
   const bool in_dev = is_device_ptr(first_v);
@@ -1234,7 +1257,10 @@ static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint
     CK(cudaStreamWaitEvent(h->stream, a.ev_h2d, 0));
     a.codes = a.d_stage + h->left;
   }
-  CK(cudaMemsetAsync(a.d_counts, 0, (size_t)nbuf * 8 * sizeof(unsigned long long), h->stream));
+  // counters zeroed off the compute stream (only chain launches sit on it in steady state)
+  CK(cudaMemsetAsync(a.d_counts, 0, (size_t)nbuf * 8 * sizeof(unsigned long long), h->aux_stream));
+  CK(cudaEventRecord(a.ev_zero, h->aux_stream));
+  CK(cudaStreamWaitEvent(h->stream, a.ev_zero, 0));
   LmsArgs la{};
   la.lut = h->d_lmslut;
   la.lcx = h->lms_lcx;
@@ -1316,6 +1342,7 @@ extern "C" kk_status kk_rx_sync(kk_rx_t* h, kk_rx_counts* out_per_buf, int64_t m
     h->a_deferred = -1;
   }
   CK(cudaStreamSynchronize(h->stream));
+  if (h->aux_stream) CK(cudaStreamSynchronize(h->aux_stream));
   for (int k = 0; k < h->a_norder; ++k) slot_harvest(h, h->aslot[h->a_order[k]]);
   h->a_norder = 0;
   const int64_t n = (int64_t)h->a_counts.size();

@@ -6,6 +6,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+import time  # noqa: E402
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
@@ -77,3 +78,18 @@ span = (prev_end - t0) / 1e3
 print(f"span {span:.3f} ms for {S} steps = {span / S:.4f} ms/step; device gaps {tot_gap / 1e3:.3f} ms; "
       f"chain launches {len(chain)} avg {np.mean(chain) / 1e3:.4f} ms min {np.min(chain) / 1e3:.4f} max {np.max(chain) / 1e3:.4f}")
 print("chain durations (ms):", " ".join(f"{c / 1e3:.3f}" for c in chain))
+
+# the same loop timed with CUDA events and host wall clock, without the profiler
+for rep in range(2):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter() if "time" in globals() else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cur)
+    for s in range(S):
+        b0 = (s * B) % P
+        rx.seek(b0)
+        sub(s, b0)
+    rx.sync()
+    e1.record(cur)
+    torch.cuda.synchronize()
+    print(f"events: {e0.elapsed_time(e1) / S:.4f} ms/step")
