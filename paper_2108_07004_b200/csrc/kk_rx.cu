@@ -51,7 +51,7 @@ struct AsyncSlot {
   const int16_t* codes = nullptr;           // device samples of buffer 0 of the batch
   uint8_t* out_dev = nullptr;               // where the chain writes labels
   uint8_t* out_host = nullptr;              // host destination (D2H after the chain) or NULL
-  cudaEvent_t ev_lms = nullptr, ev_done = nullptr, ev_h2d = nullptr, ev_copy = nullptr, ev_zero = nullptr,
+  cudaEvent_t ev_done = nullptr, ev_h2d = nullptr, ev_copy = nullptr, ev_zero = nullptr,
               ev_chain = nullptr;
   cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};  // timing: LMS start/end, chain start/end
   bool timed_lms = false, timed_chain = false;
@@ -100,7 +100,7 @@ struct kk_rx {
   int a_order[NSLOT] = {};       // slots with an issued chain, oldest first
   int a_norder = 0;
   std::vector<kk_rx_counts> a_counts;      // harvested per-buffer counters since the last sync
-  cudaStream_t lms_stream = nullptr, h2d_stream = nullptr, unpack_stream = nullptr, aux_stream = nullptr;
+  cudaStream_t h2d_stream = nullptr, unpack_stream = nullptr, aux_stream = nullptr;
   cudaEvent_t ev_in = nullptr;
   int64_t a_launches = 0;
   DecLut lut{};
@@ -449,19 +449,17 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_counts) cudaFreeHost(h->h_counts);
-  if (h->lms_stream) cudaStreamSynchronize(h->lms_stream);
   if (h->h2d_stream) cudaStreamSynchronize(h->h2d_stream);
   for (AsyncSlot& a : h->aslot) {
     void* ap[] = {a.tails, a.taps, a.d_counts, a.d_out, a.d_stage, a.d_pack};
     for (void* q : ap)
       if (q) cudaFree(q);
     if (a.h_counts) cudaFreeHost(a.h_counts);
-    for (cudaEvent_t e : {a.ev_lms, a.ev_done, a.ev_h2d, a.ev_copy, a.ev_zero, a.ev_chain, a.ev_t[0], a.ev_t[1],
+    for (cudaEvent_t e : {a.ev_done, a.ev_h2d, a.ev_copy, a.ev_zero, a.ev_chain, a.ev_t[0], a.ev_t[1],
                           a.ev_t[2], a.ev_t[3]})
       if (e) cudaEventDestroy(e);
   }
   if (h->ev_in) cudaEventDestroy(h->ev_in);
-  if (h->lms_stream) cudaStreamDestroy(h->lms_stream);
   if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
   if (h->unpack_stream) cudaStreamDestroy(h->unpack_stream);
   if (h->aux_stream) cudaStreamDestroy(h->aux_stream);
@@ -1041,8 +1039,7 @@ kk_status kk_rx_process_batch(kk_rx_t* h, const int16_t* first, int64_t nbuf, ui
 // deferred to the next submit or to kk_rx_sync.
 // ---------------------------------------------------------------------------
 static kk_status slot_reserve(kk_rx_t* h, AsyncSlot& a, int64_t nb, bool host_in, bool packed) {
-  if (!a.ev_lms) {
-    CK(cudaEventCreateWithFlags(&a.ev_lms, cudaEventDisableTiming));
+  if (!a.ev_done) {
     CK(cudaEventCreateWithFlags(&a.ev_done, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&a.ev_h2d, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&a.ev_copy, cudaEventDisableTiming));
