@@ -686,6 +686,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     const int16_t* obase = sg.codes + (int64_t)owner * a.N;
     const int64_t sbase = (int64_t)STEP * i - 256;   // owner position of stg[0] and ebuf[0]
     const float invd = 1.0f / sg.dc;
+    const float dc_invd = sg.dc * invd, vmin_invd = a.vmin * invd;
     q_step = warm ? tone_index(a, sbase) : add_mod(q_step, s3072, n32);
     const int64_t wbase = (int64_t)STEP * i - 1280;  // owner position of wstg[0]
 
@@ -773,15 +774,21 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
 #pragma unroll
           for (int j = 0; j < 48; ++j) {
             const int q = PKH + re0 + lane + 32 * j;
-            const float cvj = prek_v<PREKK>(a, src, q, sg);
-            if (PREKK && j >= 8 && j < 40 && stash) stash[32 * (j - 8) + lane] = cvj;
-            const float vv = fmaxf(cvj, a.vmin);
+            // l = lg2(max(code + d, v_min) / d), as max(code/d + 1, v_min/d): one FFMA
+            float lv;
+            if (PREKK) {
+              const float cvj = prek_v<PREKK>(a, src, q, sg);
+              if (j >= 8 && j < 40 && stash) stash[32 * (j - 8) + lane] = cvj;
+              lv = fmaxf(cvj, a.vmin) * invd;
+            } else {
+              lv = fmaxf(fmaf((float)src[q], invd, dc_invd), vmin_invd);
+            }
             // 0.5 ln 2 / 1024 (the 1/1024 of the inverse FFT folded in): applied here, or
             // (KK_F32X2) by the Hilbert mask multiply, the transform being linear
 #if KK_F32X2
-            const float l = lg2_ftz(vv * invd);
+            const float l = lg2_ftz(lv);
 #else
-            const float l = lg2_ftz(vv * invd) * (0.34657359027997264f / 1024.0f);
+            const float l = lg2_ftz(lv) * (0.34657359027997264f / 1024.0f);
 #endif
             if (j < 32) v[brev(j, 5)].x = l;        // FFT input registers are bit-reversed
             if (j >= 16) v[brev(j - 16, 5)].y = l;
@@ -834,6 +841,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           const bool cnt = !wt && sg.count_clip && (mode == SEG_APPLY || owner >= sg.ref);
           const int lim = (int)((a.N - sbase < (int64_t)(1 << 30)) ? a.N - sbase : (int64_t)(1 << 30)) - e_off;
           unsigned clip = 0;
+          float cmin = __int_as_float(0x7f800000);
           // phi to the imaginary slot of its own output (same lane writes and later reads it),
           // then one rolled loop over the 32 outputs (keeps the kernel's code small)
 #pragma unroll
@@ -863,8 +871,20 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
 #else
               dp0[o] = make_float2(fmaf(amp, cp, -sg.a_hat), amp * sp);
 #endif
-              clip += (cv < a.vmin && (allin || lane + 256 + o < lim)) ? 1u : 0u;
+              cmin = fminf(cmin, cv);
             }
+          }
+          if (cnt && cmin < a.vmin) {
+            // rare: some input of this task was clamped -- count exactly (positions < N)
+#pragma unroll 1
+            for (int t = 0; t < 16; ++t)
+              for (int hh = 0; hh < 2; ++hh) {
+                const int o = 32 * t + 512 * hh;
+                const float cv = !PREKK ? (float)sp0[o] + sg.dc
+                                 : (!warm ? reinterpret_cast<const float*>(xs)[1024 * warp + 32 * (t + 16 * hh) + lane]
+                                          : prek_v<true>(a, sp0, o, sg));
+                clip += (cv < a.vmin && (allin || lane + 256 + o < lim)) ? 1u : 0u;
+              }
           }
           if (cnt) acc_clip += clip;
           if (wt) {
