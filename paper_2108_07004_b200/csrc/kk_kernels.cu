@@ -78,6 +78,11 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+__device__ __forceinline__ float sqrt_ftz(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 // sin/cos of an angle that needs no range reduction (|x| of a few pi: the hardware
 // works in turns, so only the fp32 precision of x / 2 pi matters)
 __device__ __forceinline__ void sincos_small(float x, float* s, float* c) {
@@ -863,7 +868,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
                                : (!warm ? reinterpret_cast<const float*>(xs)[1024 * warp + 32 * (t + 16 * hh) + lane]
                                         : prek_v<true>(a, sp0, o, sg));
               const float vv = fmaxf(cv, a.vmin);
-              const float amp = vv * rsqrt_ftz(vv);
+              const float amp = sqrt_ftz(vv);
               float sp, cp;
               sincos_small(phi, &sp, &cp);  // |phi| of a few rad at most (KK phase)
 #if KK_F32X2
