@@ -260,6 +260,27 @@ __device__ __forceinline__ float prek_v(const ChainArgs& a, const int16_t* src, 
   return v;
 }
 
+// two pre-KK FIR outputs of one lane at staged indices q and q + 32 (S1's samples j and
+// j + 1), both halves through one FFMA2 per tap: per tap two loads, two exact int16->float
+// IADDs and one FADD2 (the magic number off both halves) -- bit for bit prek_v<true> twice
+__device__ __forceinline__ float2 prek_pair(const ChainArgs& a, const int16_t* src, int q, const Seg& sg) {
+  float2 acc = make_float2(sg.prek_dsum, sg.prek_dsum);
+#pragma unroll
+  for (int k = -PKH; k <= PKH; ++k)
+    if (k >= -a.prek_h && k <= a.prek_h) {
+      const float2 m = make_float2(__int_as_float((int)src[q - k] + 0x4B400000),
+                                   __int_as_float((int)src[q + 32 - k] + 0x4B400000));
+#if KK_F32X2
+      const float2 c = add2(m, make_float2(-12582912.0f, -12582912.0f));
+      acc = fma2(make_float2(a.prek[k + PKH], a.prek[k + PKH]), c, acc);
+#else
+      acc.x = fmaf(a.prek[k + PKH], m.x - 12582912.0f, acc.x);
+      acc.y = fmaf(a.prek[k + PKH], m.y - 12582912.0f, acc.y);
+#endif
+    }
+  return acc;
+}
+
 struct StepPos {
   int s, o;
   int64_t i;
@@ -776,13 +797,15 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           // pre-KK FIR: S3 needs v' at exactly this lane's j in [8, 40); keep them (x2 window,
           // free during phase H except for the warm-up task's tiles in warm steps)
           float* stash = (PREKK && !warm) ? reinterpret_cast<float*>(xs) + 1024 * warp : nullptr;
+          float2 cvp = make_float2(0.f, 0.f);
 #pragma unroll
           for (int j = 0; j < 48; ++j) {
             const int q = PKH + re0 + lane + 32 * j;
             // l = lg2(max(code + d, v_min) / d), as max(code/d + 1, v_min/d): one FFMA
             float lv;
             if (PREKK) {
-              const float cvj = prek_v<PREKK>(a, src, q, sg);
+              if ((j & 1) == 0) cvp = prek_pair(a, src, q, sg);  // samples j and j + 1
+              const float cvj = (j & 1) ? cvp.y : cvp.x;
               if (j >= 8 && j < 40 && stash) stash[32 * (j - 8) + lane] = cvj;
               lv = fmaxf(cvj, a.vmin) * invd;
             } else {

@@ -1,7 +1,9 @@
 """Summarise an `ncu --set full` report of the chain kernel for profiles/ and (optionally)
 refresh profiles/traffic.json, which bench.py reads for roofline.traffic / issue_limit.
 
-    python tools/ncu_summary.py REPORT.ncu-rep OUT.txt [--traffic profiles/traffic.json --cmd "..."]
+    python tools/ncu_summary.py REPORT.ncu-rep OUT.txt [--traffic profiles/traffic.json --samples S --cmd "..."]
+
+--samples: ADC samples the captured launch processed (buffers x 2^22; required with --traffic).
 """
 import csv
 import io
@@ -12,6 +14,9 @@ import sys
 rep, out = sys.argv[1], sys.argv[2]
 traffic = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
 cmd = sys.argv[sys.argv.index("--cmd") + 1] if "--cmd" in sys.argv else "?"
+samples = int(sys.argv[sys.argv.index("--samples") + 1]) if "--samples" in sys.argv else None
+if traffic and not samples:
+    sys.exit("--traffic needs --samples (samples processed by the captured launch)")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
@@ -48,6 +53,8 @@ if traffic:
     t = json.load(open(traffic))
     rd, wr = mb("dram__bytes_read.sum"), mb("dram__bytes_write.sum")
     t["chain_dram_bytes_per_launch"] = int(rd + wr)
+    t["chain_samples_per_launch"] = samples
+    t["chain_algorithmic_bytes_per_launch"] = int(2.25 * samples)
     t["chain_warp_inst_per_launch"] = int(float(d["smsp__inst_executed.sum"]))
     t["source"] = (f"ncu --set full of the timed combined kk_chain_kernel launch of `{cmd}`: dram__bytes_read.sum "
                    f"{rd / 1e6:.6f} MB + dram__bytes_write.sum {wr / 1e6:.6f} MB; {out}")
