@@ -7,6 +7,8 @@ if the library is missing, importing the binding raises.
 import ctypes as C
 import os
 
+import numpy as np
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkkrx.so")
 # A/B measurements of kernel variants (tools/gpu/ab.sh): another in-tree build of the same library
@@ -63,6 +65,11 @@ class KKCounts(C.Structure):
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_ if f != "reserved"}
 
+
+# numpy view of kk_rx_counts (same layout): bulk counters without per-buffer Python objects
+COUNTS_DTYPE = np.dtype([("bit_errors", "<u8"), ("sym_errors", "<u8"), ("bits", "<u8"), ("symbols", "<u8"),
+                         ("clipped_samples", "<u8"), ("gated_updates", "<u8"), ("flags", "<u4"), ("reserved", "<u4")])
+assert COUNTS_DTYPE.itemsize == C.sizeof(KKCounts)
 
 EXPORTS = {
     "kk_rx_params_default": (None, [C.POINTER(KKParams)]),

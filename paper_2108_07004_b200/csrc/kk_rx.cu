@@ -127,6 +127,7 @@ struct kk_rx {
   int64_t last_launches = 0;
   // per-kernel timing (kk_rx_set_timing): events around each launch slot of a chunk
   bool timing = false;
+  cudaEvent_t trace_ref = nullptr;  // KKRX_EVENT_TRACE diagnostics
   cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
   double kernel_ms[3] = {0, 0, 0};
   int64_t kernel_n[3] = {0, 0, 0};
@@ -1093,6 +1094,13 @@ static void slot_harvest(kk_rx_t* h, AsyncSlot& a) {
     h->kernel_ms[2] += ms;
     h->kernel_n[2] += 1;
   }
+  if (a.timed_chain && h->trace_ref) {
+    // KKRX_EVENT_TRACE=1: start/end of every chain launch relative to the first one
+    float t0 = 0.f, t1 = 0.f;
+    cudaEventElapsedTime(&t0, h->trace_ref, a.ev_t[2]);
+    cudaEventElapsedTime(&t1, h->trace_ref, a.ev_t[3]);
+    std::fprintf(stderr, "KKRX_EVENT_TRACE chain %9.4f -> %9.4f ms (%.4f)\n", t0, t1, t1 - t0);
+  }
   a.timed_lms = a.timed_chain = false;
   for (int64_t b = 0; b < a.nb; ++b) {
     const unsigned long long* c = a.h_counts + 8 * b;
@@ -1150,6 +1158,10 @@ static kk_status issue_chain(kk_rx_t* h, int p, int t, const LmsArgs* la) {
     CK(e);
   }
   if (h->timing) CK(cudaEventRecord(ap.ev_t[2], h->stream));
+  if (h->timing && !h->trace_ref && std::getenv("KKRX_EVENT_TRACE")) {
+    CK(cudaEventCreate(&h->trace_ref));
+    CK(cudaEventRecord(h->trace_ref, h->stream));
+  }
   CK(chain_launch(h, ca, grid, h->stream));
   if (h->timing) CK(cudaEventRecord(ap.ev_t[3], h->stream));
   ap.timed_chain = h->timing;

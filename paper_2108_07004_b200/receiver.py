@@ -11,7 +11,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from ._lib import KKCounts, KKParams, check
+from ._lib import COUNTS_DTYPE, KKCounts, KKParams, check
 
 
 def _ptr(obj):
@@ -102,7 +102,7 @@ class KKReceiver:
     def seek(self, buffer_index):
         check(self._lib.kk_rx_seek(self.h, int(buffer_index)), "kk_rx_seek")
 
-    def process_batch(self, stream, offset, nbuf, out=None):
+    def process_batch(self, stream, offset, nbuf, out=None, as_array=False):
         """stream: int16 torch tensor (cuda or pinned cpu) or NumPy array holding
         the contiguous sample stream; offset: index of buffer 0's first sample.
         out: uint8 tensor/array of nbuf*N/4 labels or None.  Returns a list of
@@ -112,11 +112,12 @@ class KKReceiver:
         optr = None
         if out is not None:
             optr, _ = _ptr(out)
-        cnt = (KKCounts * int(nbuf))()
+        buf = self._counts_buf(nbuf)
         check(self._lib.kk_rx_process_batch(self.h, C.c_void_p(base + 2 * int(offset)), int(nbuf),
-                                            C.c_void_p(optr) if optr is not None else None, cnt),
-              "kk_rx_process_batch")
-        return [c.as_dict() for c in cnt]
+                                            C.c_void_p(optr) if optr is not None else None,
+                                            buf.ctypes.data_as(C.POINTER(KKCounts))), "kk_rx_process_batch")
+        arr = buf[:int(nbuf)].copy()
+        return arr if as_array else self._as_dicts(arr)
 
     def submit_batch(self, stream, offset, nbuf, out=None):
         """Asynchronous kk_rx_submit_batch: enqueue nbuf buffers (see process_batch for
@@ -142,12 +143,25 @@ class KKReceiver:
                                                     C.c_void_p(optr) if optr is not None else None),
               "kk_rx_submit_batch_packed12")
 
-    def sync(self, max_out=1 << 16):
-        """kk_rx_sync: wait for every submitted batch; per-buffer counter dicts in order."""
-        cnt = (KKCounts * int(max_out))()
+    def _counts_buf(self, n):
+        if getattr(self, "_cbuf", None) is None or len(self._cbuf) < n:
+            self._cbuf = np.zeros(max(int(n), 1), dtype=COUNTS_DTYPE)
+        return self._cbuf
+
+    @staticmethod
+    def _as_dicts(arr):
+        names = [f for f in COUNTS_DTYPE.names if f != "reserved"]
+        return [{f: int(r[f]) for f in names} for r in arr]
+
+    def sync(self, max_out=1 << 16, as_array=False):
+        """kk_rx_sync: wait for every submitted batch; per-buffer counters in order, as dicts
+        or (as_array) one numpy structured array (COUNTS_DTYPE, no per-buffer objects)."""
+        buf = self._counts_buf(max_out)
         n = C.c_int64()
-        check(self._lib.kk_rx_sync(self.h, cnt, int(max_out), C.byref(n)), "kk_rx_sync")
-        return [cnt[i].as_dict() for i in range(min(n.value, max_out))]
+        check(self._lib.kk_rx_sync(self.h, buf.ctypes.data_as(C.POINTER(KKCounts)), int(max_out), C.byref(n)),
+              "kk_rx_sync")
+        arr = buf[:min(n.value, max_out)].copy()
+        return arr if as_array else self._as_dicts(arr)
 
     def set_dc_offset(self, dc_offset):
         check(self._lib.kk_rx_set_dc_offset(self.h, float(dc_offset)), "kk_rx_set_dc_offset")
