@@ -90,3 +90,22 @@ def test_cufft_comparison_library_exports(root):
     assert lib.kk_cmp_create(C.byref(h), 1 << 16, 1, 1000.0, 10.0, 1.0, 541065, fp, 202) == -1         # fir_len
     assert lib.kk_cmp_create(C.byref(h), 1 << 16, 0, 1000.0, 10.0, 1.0, 541065, fp, 203) == -1         # batch
     assert lib.kk_cmp_destroy(None) == 0
+
+
+def test_new_entry_points_reject_bad_arguments():
+    """The sweep / CSPR / frame-sync / training calls validate their arguments before any
+    CUDA work (KK_EINVAL with a NULL handle or impossible sizes; no GPU needed)."""
+    lib = _lib.load()
+    f = np.ones(4, np.float32)
+    fp = f.ctypes.data_as(C.POINTER(C.c_float))
+    cnt = (_lib.KKCounts * 4)()
+    best = C.c_int()
+    k = C.c_int64()
+    assert lib.kk_rx_set_cspr(None, 12.0) == _lib.KK_EINVAL
+    assert lib.kk_rx_sweep(None, None, 1, fp, None, 4, cnt, C.byref(best)) == _lib.KK_EINVAL
+    assert lib.kk_rx_dc_sweep(None, None, 1, fp, 4, cnt, C.byref(best)) == _lib.KK_EINVAL
+    assert lib.kk_rx_frame_sync(None, None, 0, 2048, C.byref(k), None, None) == _lib.KK_EINVAL
+    assert lib.kk_rx_train_fir(None, None, fp, 32, 2, 0.0, fp) == _lib.KK_EINVAL
+    assert lib.kk_rx_train_taps(None, None, 16, fp) == _lib.KK_EINVAL
+    assert lib.kk_rx_set_dc_offset(None, 100.0) == _lib.KK_EINVAL
+    assert lib.kk_rx_last_error(None)
