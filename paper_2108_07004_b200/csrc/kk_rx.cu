@@ -1770,8 +1770,7 @@ extern "C" kk_status kk_gmi_awgn(const float* points, const uint8_t* labels, int
   uint8_t* d_l = nullptr;
   double2* d_n = nullptr;
   double *d_w = nullptr, *d_o = nullptr;
-  kk_rx_t* h = nullptr;  // for CK() (no handle here)
-  (void)h;
+  [[maybe_unused]] kk_rx_t* h = nullptr;  // for CK() (no handle here)
   auto release = [&]() {
     void* ptrs[] = {d_p, d_l, d_n, d_w, d_o};
     for (void* q : ptrs)
