@@ -42,6 +42,7 @@ FLOP_PER_SA_CHAIN = 240.0        # whole chain (+ WL apply 16, decision ~5, upda
 # FP32 SIMT peak derived from the unit counts and max clock (B200_PROFILING.md):
 # 148 SMs x 128 FP32 lanes x 2 flop (FFMA) x 1.965 GHz
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+FP32_MEASURED_TFLOPS = 7.652 * 32 * 2 * 148 / 1e3  # tools/microbench/f32x2_rate.cu, 32 warps/SM
 
 
 def _env_int(k, d):
@@ -430,6 +431,10 @@ def run_gpu(args):
                      "hbm_algorithmic_bytes_per_launch": HBM_BYTES_PER_SA * B * N,
                      "hbm_achieved_gbs": HBM_BYTES_PER_SA * B * N / (ch_avg_ms / 1e3) / 1e9,
                      "peak_basis": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (derived, DESIGN.md)",
+                     "peak_measured_fp32": FP32_MEASURED_TFLOPS,
+                     "peak_measured_basis": "FFMA throughput microbenchmark on this B200 (tools/microbench/f32x2_rate.cu: "
+                                            "7.652 warp-FFMA/ns/SM x 32 lanes x 2 flop x 148 SMs)",
+                     "frac_of_measured": achieved_tf / FP32_MEASURED_TFLOPS,
                      "issue_limit": issue_limit(traffic, B * N, ch_avg_ms)},
         "kernel_ms_per_step": {"chain": ch_avg_ms, "lms_overlapped": lms_avg},
         "pipeline": ("kk_rx_submit_batch per step + one kk_rx_sync: the LMS update pass of batch j (one SM, "
