@@ -127,6 +127,7 @@ struct ChainArgs {
   // the LMS update pass of the next batch as extra CTAs of this launch (the last lms_ctas
   // blocks; lane-per-chain body, waits on tail_ctr for the tails this launch computes)
   int32_t lms_ctas, lms_mode;
+  int32_t lms_warp;  // extra CTAs run the warp-per-chain update pass (one chain each) instead of lanes
   LmsArgs lms;
   // pre-KK intensity equaliser: v' = sum_{k=-h..h} prek[k+h] code[n-k] + dsum,
   // dsum = d * sum(prek) per segment (Seg.prek_dsum); prek_h < 0: off (the plain kernel)

@@ -46,6 +46,8 @@ constexpr size_t SMEM_GROUP = SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT + 64 + 1
 constexpr size_t CHAIN_SMEM = SMEM_SHARED + NGROUP * SMEM_GROUP;
 static_assert(SMEM_GROUP % 16 == 0 && SMEM_SHARED % 16 == 0, "16-B aligned regions");
 static_assert(LMS_LUT_G * LMS_LUT_G * 8 + 129 * 8 <= SMEM_SHARED + NGROUP * SMEM_GROUP, "LMS CTAs fit the chain smem");
+static_assert(LMS_LUT_G * LMS_LUT_G * 8 + (2 * 5632 + 16) * 8 + 130 * 8 + 8 <= SMEM_SHARED + NGROUP * SMEM_GROUP,
+              "warp-per-chain LMS CTAs (table + x2 window + points + mbarrier) fit the chain smem");
 static_assert(WARM2 * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-up codes + tile must fit the x2 window");
 constexpr int WOFF = WARM2 * (int)sizeof(int16_t) / (int)sizeof(float2);  // float2 offset of the warm-up tile in xs
 static_assert(TILE * sizeof(float) <= EQ_KEEP * sizeof(float2), "transpose tile must fit an EQ stride of ebuf");
@@ -210,6 +212,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
@@ -316,6 +321,7 @@ __device__ __forceinline__ StepPos decode_step(const ChainArgs& a, int64_t g) {
 }
 
 constexpr size_t LMS_LUT_BYTES = (size_t)LMS_LUT_G * LMS_LUT_G * sizeof(float2);
+constexpr int LMS_CHUNK = 5632;  // update steps per shared-memory window of x2 (kk_lms_kernel / lms_warp_body)
 
 // ---------------------------------------------------------------------------
 // Kernel 2b: LMS update pass with one LANE per chain (up to 512 chains per CTA,
@@ -556,6 +562,31 @@ __global__ void __launch_bounds__(LMSL_MAXW * 32) kk_lms_lanes_kernel(LmsArgs a)
 //   phase E: 4 static-EQ blocks (one per warp): S4 -> x2 (smem or HBM)
 //   phase A: 768 symbols of S5' + S6 + S7 (APPLY segments)
 // ---------------------------------------------------------------------------
+template <int MODE>
+__device__ __forceinline__ void lms_warp_body(const LmsArgs& a, unsigned char* lms_smem, float2* s_pts,
+                                              uint64_t* s_barp, int c, int lane);
+
+// few chains (ChainArgs.lms_warp): one chain per extra CTA, warp 0 runs the
+// warp-per-chain update pass (x2 window in shared memory) after the tails are published
+__device__ __forceinline__ void lms_warp_cta(const LmsArgs& a, unsigned char* smem, int c, int mode) {
+  float2* sp = reinterpret_cast<float2*>(smem + LMS_LUT_BYTES + (2 * LMS_CHUNK + 16) * sizeof(float2));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sp + 130);
+  const int lane = (int)threadIdx.x;
+  if (a.wait_ctr) {
+    if (lane == 0)
+      while (ld_acquire_u64(a.wait_ctr) < a.wait_target) __nanosleep(200);
+    __syncwarp();
+  }
+  if (mode == 1)
+    lms_warp_body<1>(a, smem, sp, bar, c, lane);
+  else if (mode == 2)
+    lms_warp_body<2>(a, smem, sp, bar, c, lane);
+  else
+    lms_warp_body<0>(a, smem, sp, bar, c, lane);
+  __syncwarp();
+  if (lane == 0) mbar_inval(bar);  // the memory becomes chain-kernel shared memory next
+}
+
 template <bool PREKK>
 __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(ChainArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -563,7 +594,12 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     // the next batch's LMS update pass: these CTAs come last in the launch order and wait
     // only for tail steps of this launch, which the chain CTAs never wait for.  Afterwards
     // they join the chain work (dynamic schedule only) with the shared memory rebuilt
-    lms_lanes_body(a.lms, smem_raw, (int)blockIdx.x - ((int)gridDim.x - a.lms_ctas), a.lms_mode);
+    const int lblk = (int)blockIdx.x - ((int)gridDim.x - a.lms_ctas);
+    if (a.lms_warp) {
+      if (threadIdx.x < 32 && lblk < a.lms.nchains) lms_warp_cta(a.lms, smem_raw, lblk, a.lms_mode);
+    } else {
+      lms_lanes_body(a.lms, smem_raw, lblk, a.lms_mode);
+    }
     if (a.work_ctr == nullptr) return;
     __syncthreads();
   }
@@ -1181,24 +1217,21 @@ cudaError_t launch_chain(const ChainArgs& a, int grid, cudaStream_t s) {
 //    index on ties), from which k1, D1 and D2 (second-smallest distance) follow
 //    exactly as in the oracle; cells with longer lists fall back to brute force.
 // ---------------------------------------------------------------------------
-constexpr int LMS_CHUNK = 5632;  // update steps per shared-memory window of x2
 constexpr size_t LMS_SMEM_MAX = 220 * 1024;  // + static smem <= 227 KB
 static_assert(LMS_LUT_BYTES + (2 * LMS_CHUNK + 16) * sizeof(float2) <= LMS_SMEM_MAX, "LMS smem budget");
 
 
-// one warp per chain; shared memory = [LUT (not in PILOT mode)] [x2 window of <= LMS_CHUNK steps]
+// one warp per chain; shared memory = [LUT (not in PILOT mode)] [x2 window of <= LMS_CHUNK steps].
+// The body runs in kk_lms_kernel (one 32-thread CTA per chain) and in warp 0 of extra CTAs
+// of a chain launch (streaming pipeline with few chains: ChainArgs.lms_warp).
 template <int MODE>  // 0: DD soft gate, 1: PILOT (known pattern), 2: DD hard (gamma = 1)
-__global__ void __launch_bounds__(32) kk_lms_kernel(LmsArgs a) {
-  extern __shared__ __align__(128) unsigned char lms_smem[];
-  __shared__ float2 s_pts[129];
-  __shared__ __align__(8) uint64_t s_bar;
+__device__ __forceinline__ void lms_warp_body(const LmsArgs& a, unsigned char* lms_smem, float2* s_pts,
+                                              uint64_t* s_barp, int c, int lane) {
+  uint64_t& s_bar = *s_barp;
   constexpr size_t LUTB = (MODE == 1) ? 0 : LMS_LUT_BYTES;
   const float2* s_lut = reinterpret_cast<const float2*>(lms_smem);
   float2* s_win = reinterpret_cast<float2*>(lms_smem + LUTB);
   const float INF = __int_as_float(0x7f800000);
-  const int lane = threadIdx.x;
-  const int c = blockIdx.x;
-  if (c >= a.nchains) return;
   for (int i = lane; i < 129; i += 32) s_pts[i] = (i < a.m) ? a.pts[i] : make_float2(INF, INF);
   const int b = c / a.nsub, sblk = c - b * a.nsub;
   const int64_t n0l = (int64_t)sblk * a.L - a.K;       // first update symbol, buffer-relative
@@ -1422,6 +1455,15 @@ __global__ void __launch_bounds__(32) kk_lms_kernel(LmsArgs a) {
     for (int k = 0; k < 4; ++k) bad |= !isfinite(A[k] + B[k] + C[k] + D[k]);
     if (bad) atomicOr(&a.counts[b * 8 + C_FLAGS], 1ull);
   }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(32) kk_lms_kernel(LmsArgs a) {
+  extern __shared__ __align__(128) unsigned char lms_smem[];
+  __shared__ float2 s_pts[129];
+  __shared__ __align__(8) uint64_t s_bar;
+  if ((int)blockIdx.x >= a.nchains) return;
+  lms_warp_body<MODE>(a, lms_smem, s_pts, &s_bar, (int)blockIdx.x, (int)threadIdx.x);
 }
 
 static size_t lms_smem_bytes(int mode, int K) {

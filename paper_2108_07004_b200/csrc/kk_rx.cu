@@ -1126,6 +1126,8 @@ static void slot_harvest(kk_rx_t* h, AsyncSlot& a) {
 
 // the fused chain of slot p (APPLY), optionally preceded in the same launch by the
 // x2 tails of slot t's batch (a leading SEG_X2_TAIL segment, published via the counter)
+constexpr int LMS_WARP_MAX_CHAINS = 60;  // measured crossover (streaming small batches)
+
 static kk_status issue_chain(kk_rx_t* h, int p, int t, const LmsArgs* la) {
   AsyncSlot& ap = h->aslot[p];
   ChainArgs ca{};
@@ -1141,8 +1143,12 @@ static kk_status issue_chain(kk_rx_t* h, int p, int t, const LmsArgs* la) {
     ca.aligned16 = ca.aligned16 && ((uintptr_t)at.codes % 16) == 0;
     if (la) {  // batch t's update pass rides along as the last CTAs of this launch
       ca.lms = *la;
-      ca.lms_ctas = lms_lanes_ctas(la->nchains);
       ca.lms_mode = (la->mode == 1) ? 1 : (la->mode == 2 || !(la->inv_tau > 0.f)) ? 2 : 0;
+      // few chains: the chain work of the launch is short, so the one-SM lane-per-chain pass
+      // (~1.2 ms for 4096 steps) would set the launch time; one warp-per-chain CTA per chain
+      // (~0.3 ms, x2 window in shared memory) instead, each joining the chain work afterwards
+      ca.lms_warp = (la->nchains <= LMS_WARP_MAX_CHAINS) ? 1 : 0;
+      ca.lms_ctas = ca.lms_warp ? la->nchains : lms_lanes_ctas(la->nchains);
     }
   }
   ca.seg[ns++] = Seg{0, (int32_t)ap.nb, 0, S, SEG_APPLY, 1, 0, 0, nullptr, ap.out_dev, ap.d_counts, ap.taps, ap.n_off0,
