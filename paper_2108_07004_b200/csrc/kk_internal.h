@@ -70,6 +70,7 @@ struct Seg {
 //                     nearest anywhere in the cell; word = ~0u: brute force
 // The outermost ring of cells is always SLOW/brute (y is clamped into the grid).
 constexpr int LMS_LUT_G = 128;
+constexpr int GRAM_SPLIT = 16;  // train_fir: training symbols split over grid.z (partial R/b planes, fixed-order sum)
 constexpr uint32_t LMS_BRUTE = 0xffffffffu;
 
 

@@ -1578,9 +1578,14 @@ __global__ void __launch_bounds__(256) kk_gram_kernel(const float2* __restrict__
   const bool rhs = (int)blockIdx.y == nt;
   if (rhs && blockIdx.x > 0) return;
   const int half = ntap / 2;
+  // this CTA's slice of the training symbols and its partial-sum plane
+  const int chunk = (n_count + GRAM_SPLIT - 1) / GRAM_SPLIT;
+  const int nlo = (int)blockIdx.z * chunk, nhi = min(n_count, nlo + chunk);
+  R += (int64_t)blockIdx.z * ntap * ntap;
+  bvec += (int64_t)blockIdx.z * ntap;
   double sr = 0.0, si = 0.0;
   if (!rhs && t1 < ntap && t2 < ntap && t2 >= t1) {
-    for (int n = 0; n < n_count; ++n) {
+    for (int n = nlo; n < nhi; ++n) {
       const int64_t base = pos_first + 4 * (int64_t)n + half;
       const float2 a1 = es[base - t1], a2 = es[base - t2];
       // conj(a1) * a2
@@ -1592,7 +1597,7 @@ __global__ void __launch_bounds__(256) kk_gram_kernel(const float2* __restrict__
   } else if (rhs && threadIdx.x < GRAM_T) {
     for (int t = threadIdx.x; t < ntap; t += GRAM_T) {
       double br = 0.0, bi = 0.0;
-      for (int n = 0; n < n_count; ++n) {
+      for (int n = nlo; n < nhi; ++n) {
         const float2 a = es[pos_first + 4 * (int64_t)n + half - t];
         const float2 s = sym[n];
         br += (double)a.x * s.x + (double)a.y * s.y;
@@ -1604,10 +1609,30 @@ __global__ void __launch_bounds__(256) kk_gram_kernel(const float2* __restrict__
 }
 
 // (R + ridge * tr(R)/n * I) h = b, R Hermitian positive definite (n <= 256), in place;
-// one CTA of 256 threads, shared-memory-free (R in global / L2), fp64.
-__global__ void __launch_bounds__(256) kk_chol_solve_kernel(double2* __restrict__ R, double2* __restrict__ b, int n,
-                                                            double ridge, float* __restrict__ out) {
+// one CTA of 1024 threads, shared-memory-free (R in global / L2), fp64.  R and b arrive as
+// GRAM_SPLIT partial planes, summed here in a fixed order (deterministic).
+__global__ void __launch_bounds__(1024) kk_chol_solve_kernel(double2* __restrict__ R, double2* __restrict__ b, int n,
+                                                             double ridge, float* __restrict__ out) {
   __shared__ double s_tr;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+    double2 t = R[i];
+    for (int z = 1; z < GRAM_SPLIT; ++z) {
+      const double2 q = R[(int64_t)z * n * n + i];
+      t.x += q.x;
+      t.y += q.y;
+    }
+    R[i] = t;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double2 t = b[i];
+    for (int z = 1; z < GRAM_SPLIT; ++z) {
+      const double2 q = b[(int64_t)z * n + i];
+      t.x += q.x;
+      t.y += q.y;
+    }
+    b[i] = t;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     double tr = 0.0;
     for (int k = 0; k < n; ++k) tr += R[(int64_t)k * n + k].x;
@@ -1734,10 +1759,10 @@ cudaError_t launch_frame_sync(const float2* es, int64_t es_first, int L, const u
 cudaError_t launch_train_fir(const float2* es, int64_t pos_first, const float2* sym, int n_count, int ntap, double ridge,
                              double2* R, double2* b, float* out, cudaStream_t s) {
   const int nt = (ntap + GRAM_T - 1) / GRAM_T;
-  kk_gram_kernel<<<dim3(nt, nt + 1), GRAM_T * GRAM_T, 0, s>>>(es, pos_first, sym, n_count, ntap, R, b);
+  kk_gram_kernel<<<dim3(nt, nt + 1, GRAM_SPLIT), GRAM_T * GRAM_T, 0, s>>>(es, pos_first, sym, n_count, ntap, R, b);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  kk_chol_solve_kernel<<<1, 256, 0, s>>>(R, b, ntap, ridge, out);
+  kk_chol_solve_kernel<<<1, 1024, 0, s>>>(R, b, ntap, ridge, out);
   return cudaGetLastError();
 }
 

@@ -128,6 +128,10 @@ struct kk_rx {
   // per-kernel timing (kk_rx_set_timing): events around each launch slot of a chunk
   bool timing = false;
   cudaEvent_t trace_ref = nullptr;  // KKRX_EVENT_TRACE diagnostics
+  // init-time work buffers (train_fir / train_taps / frame_sync), grown on demand, kept
+  // until destroy: cudaMalloc/cudaFree per call cost more than the work itself
+  void* iw[8] = {};
+  size_t iw_cap[8] = {};
   cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
   double kernel_ms[3] = {0, 0, 0};
   int64_t kernel_n[3] = {0, 0, 0};
@@ -449,6 +453,8 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
                   h->d_x2full, h->d_es,     h->d_stage[0], h->d_stage[1]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (void* q : h->iw)
+    if (q) cudaFree(q);
   if (h->h_counts) cudaFreeHost(h->h_counts);
   if (h->h2d_stream) cudaStreamSynchronize(h->h2d_stream);
   for (AsyncSlot& a : h->aslot) {
@@ -1492,6 +1498,19 @@ static kk_status one_buffer_stages(kk_rx_t* h, const int16_t* codes, float2* x2_
   return KK_OK;
 }
 
+enum { IW_X2 = 0, IW_ES, IW_R, IW_B, IW_SYM, IW_OUT, IW_CVAL, IW_SMALL };
+// a cached init-time work buffer of at least `bytes` (nullptr if the allocation fails)
+static void* iw_get(kk_rx_t* h, int slot, size_t bytes) {
+  if (h->iw_cap[slot] < bytes) {
+    if (h->iw[slot]) cudaFree(h->iw[slot]);
+    h->iw[slot] = nullptr;
+    h->iw_cap[slot] = 0;
+    if (cudaMalloc(&h->iw[slot], bytes) != cudaSuccess) return nullptr;
+    h->iw_cap[slot] = bytes;
+  }
+  return h->iw[slot];
+}
+
 extern "C" kk_status kk_rx_train_fir(kk_rx_t* h, const int16_t* buffer, const float* symbols, int64_t n_first,
                                      int64_t n_count, double ridge, float* out_fir) {
   if (!h || !buffer || !symbols || !out_fir || n_count <= 0) return fail(KK_EINVAL, "bad arguments");
@@ -1503,22 +1522,19 @@ extern "C" kk_status kk_rx_train_fir(kk_rx_t* h, const int16_t* buffer, const fl
   const int16_t* dev0 = nullptr;
   kk_status st = stage_one(h, buffer, &tmp, &dev0);
   if (st != KK_OK) return st;
-  float2 *x2 = nullptr, *es = nullptr, *sym = nullptr;
-  double2 *R = nullptr, *b = nullptr;
-  float* out = nullptr;
   auto release = [&]() {
-    void* ptrs[] = {tmp, x2, es, sym, R, b, out};
-    for (void* q : ptrs)
-      if (q) cudaFree(q);
+    if (tmp) cudaFree(tmp);
   };
   cudaError_t e = cudaSuccess;
   const int ntap = 203;
-  if (e == cudaSuccess) e = cudaMalloc(&x2, (size_t)(h->x2h + h->N / 2 + 64) * sizeof(float2));
-  if (e == cudaSuccess) e = cudaMalloc(&es, (size_t)h->N * sizeof(float2));
-  if (e == cudaSuccess) e = cudaMalloc(&sym, (size_t)n_count * sizeof(float2));
-  if (e == cudaSuccess) e = cudaMalloc(&R, (size_t)ntap * ntap * sizeof(double2));
-  if (e == cudaSuccess) e = cudaMalloc(&b, (size_t)ntap * sizeof(double2));
-  if (e == cudaSuccess) e = cudaMalloc(&out, 2 * ntap * sizeof(float));
+  auto* x2 = static_cast<float2*>(iw_get(h, IW_X2, (size_t)(h->x2h + h->N / 2 + 64) * sizeof(float2)));
+  auto* es = static_cast<float2*>(iw_get(h, IW_ES, (size_t)h->N * sizeof(float2)));
+  auto* sym = static_cast<float2*>(iw_get(h, IW_SYM, (size_t)n_count * sizeof(float2)));
+  // GRAM_SPLIT partial planes of R and b (kk_gram_kernel), summed by the solver
+  auto* R = static_cast<double2*>(iw_get(h, IW_R, (size_t)GRAM_SPLIT * ntap * ntap * sizeof(double2)));
+  auto* b = static_cast<double2*>(iw_get(h, IW_B, (size_t)GRAM_SPLIT * ntap * sizeof(double2)));
+  auto* out = static_cast<float*>(iw_get(h, IW_OUT, 2 * ntap * sizeof(float)));
+  if (!x2 || !es || !sym || !R || !b || !out) e = cudaErrorMemoryAllocation;
   if (e == cudaSuccess) e = cudaMemcpyAsync(sym, symbols, (size_t)n_count * sizeof(float2), cudaMemcpyHostToDevice, h->stream);
   if (e != cudaSuccess) {
     release();
@@ -1553,19 +1569,17 @@ extern "C" kk_status kk_rx_frame_sync(kk_rx_t* h, const int16_t* buffer, int64_t
   const int16_t* dev0 = nullptr;
   kk_status st = stage_one(h, buffer, &tmp, &dev0);
   if (st != KK_OK) return st;
-  float2 *x2 = nullptr, *es = nullptr, *cval = nullptr;
-  unsigned long long* best = nullptr;
-  double* sum2 = nullptr;
   auto release = [&]() {
-    void* ptrs[] = {tmp, x2, es, cval, best, sum2};
-    for (void* q : ptrs)
-      if (q) cudaFree(q);
+    if (tmp) cudaFree(tmp);
   };
-  cudaError_t e = cudaMalloc(&x2, (size_t)(h->x2h + h->N / 2 + 64) * sizeof(float2));
-  if (e == cudaSuccess) e = cudaMalloc(&es, (size_t)h->N * sizeof(float2));
-  if (e == cudaSuccess && peak) e = cudaMalloc(&cval, (size_t)h->P * sizeof(float2));
-  if (e == cudaSuccess) e = cudaMalloc(&best, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMalloc(&sum2, sizeof(double));
+  cudaError_t e = cudaSuccess;
+  auto* x2 = static_cast<float2*>(iw_get(h, IW_X2, (size_t)(h->x2h + h->N / 2 + 64) * sizeof(float2)));
+  auto* es = static_cast<float2*>(iw_get(h, IW_ES, (size_t)h->N * sizeof(float2)));
+  float2* cval = peak ? static_cast<float2*>(iw_get(h, IW_CVAL, (size_t)h->P * sizeof(float2))) : nullptr;
+  auto* small = static_cast<unsigned char*>(iw_get(h, IW_SMALL, 256));
+  auto* best = reinterpret_cast<unsigned long long*>(small);
+  auto* sum2 = reinterpret_cast<double*>(small + 16);
+  if (!x2 || !es || (peak && !cval) || !small) e = cudaErrorMemoryAllocation;
   if (e == cudaSuccess) e = cudaMemsetAsync(best, 0, sizeof(unsigned long long), h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(sum2, 0, sizeof(double), h->stream);
   if (e != cudaSuccess) {
@@ -1633,11 +1647,12 @@ extern "C" kk_status kk_rx_train_taps(kk_rx_t* h, const int16_t* buffer, int32_t
   const int16_t* dev0 = nullptr;
   kk_status st = stage_one(h, buffer, &tmp, &dev0);
   if (st != KK_OK) return st;
-  float2 *x2 = nullptr, *taps = nullptr;
-  unsigned long long* cnt = nullptr;
-  cudaError_t e = cudaMalloc(&x2, (size_t)(h->x2h + h->N / 2 + 64) * sizeof(float2));
-  if (e == cudaSuccess) e = cudaMalloc(&taps, 8 * sizeof(float2));
-  if (e == cudaSuccess) e = cudaMalloc(&cnt, 8 * sizeof(unsigned long long));
+  cudaError_t e = cudaSuccess;
+  auto* x2 = static_cast<float2*>(iw_get(h, IW_X2, (size_t)(h->x2h + h->N / 2 + 64) * sizeof(float2)));
+  auto* small = static_cast<unsigned char*>(iw_get(h, IW_SMALL, 256));
+  auto* taps = reinterpret_cast<float2*>(small);                      // 8 float2
+  auto* cnt = reinterpret_cast<unsigned long long*>(small + 128);     // 8 counters
+  if (!x2 || !small) e = cudaErrorMemoryAllocation;
   if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), h->stream);
   if (e == cudaSuccess) {
     st = one_buffer_stages(h, dev0, x2, nullptr);
@@ -1678,7 +1693,7 @@ extern "C" kk_status kk_rx_train_taps(kk_rx_t* h, const int16_t* buffer, int32_t
     h->sticky = KK_ECUDA;
     st = fail(KK_ECUDA, std::string("kk_rx_train_taps: ") + cudaGetErrorString(e));
   }
-  void* ptrs[] = {tmp, x2, taps, cnt};
+  void* ptrs[] = {tmp};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   return st;
