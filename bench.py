@@ -415,10 +415,11 @@ def run_gpu(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.workload}: GS-128, CSPR 16 dB, two-sided ASE at OSNR 35 dB, "
                                f"2^22-sample 12-bit buffers, {B} buffers/step/GPU, pool of {P} distinct buffers "
-                               f"cycled (inputs+x2 scratch > L2 per step)",
+                               f"cycled (inputs > L2 per step)",
                    "buffer_len": N, "buffers_per_step_per_gpu": B, "parallelism": f"buffer-sharded x{world}",
-                   "l2": "inputs larger than L2 (pool %.0f MiB + x2 scratch %.0f MiB per step)" % (
-                       P * N * 2 / 2**20, B * N / 2 * 8 / 2**20)},
+                   "l2": "inputs larger than L2: each step reads %d x %.0f MiB = %.0f MiB of int16 codes from "
+                         "distinct device memory (the %d-buffer pool laid out cycled into a %d-buffer stream); "
+                         "L2 is 126 MB" % (B, N * 2 / 2**20, B * N * 2 / 2**20, P, P + B)},
         "gbaud_equiv": value / 4.0,
         "hbm_fraction": value * HBM_BYTES_PER_SA / hbm,
         "fp32_fraction_chain": value * FLOP_PER_SA_CHAIN / (FP32_PEAK_TFLOPS * 1e3),
