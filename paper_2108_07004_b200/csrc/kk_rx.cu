@@ -455,6 +455,7 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
     if (p) cudaFree(p);
   for (void* q : h->iw)
     if (q) cudaFree(q);
+  if (h->trace_ref) cudaEventDestroy(h->trace_ref);
   if (h->h_counts) cudaFreeHost(h->h_counts);
   if (h->h2d_stream) cudaStreamSynchronize(h->h2d_stream);
   for (AsyncSlot& a : h->aslot) {
