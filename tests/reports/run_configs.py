@@ -11,7 +11,9 @@ Config-specific checks: C1 zero errors; C2 BER vs the one-sided closed form;
 C4 Q above the 20 % HDFEC threshold 6.70 dB; C3 the CSPR trade-off
 is reported.
 
-    python tools/run_configs.py [--out gpurun_out/configs_report.json] [--quick]
+    python tests/reports/run_configs.py [--out gpurun_out/configs_report.json] [--quick]
+
+Lives under tests/ because it runs the float64 oracle (test infrastructure only).
 
 Pools: C4 uses 32 distinct buffers cycled to 256 and C5 64 cycled to 256 (the
 synthesis of 256 distinct two-sided-noise buffers alone takes ~15 CPU-minutes);
@@ -28,7 +30,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # tests/reports/ -> repo root
 sys.path.insert(0, ROOT)
 
 from synth import configs  # noqa: E402
