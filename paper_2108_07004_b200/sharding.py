@@ -3,9 +3,10 @@
 The KK chain shards buffer-by-buffer: the outputs of buffer b depend only on the
 raw window [bN - left, (b+1)N + right) (adaptive taps restart per sub-block,
 reading R10; the tone phase is buffer-local, reading R7), so ranks process
-disjoint buffer ranges with no data-path collective.  The only collective is
-one all_reduce(SUM) of the int64 error counters (and MAX of elapsed time) at
-the end of a run or report window -- torch.distributed over NCCL on B200s,
+disjoint buffer ranges.  The collectives: one all_reduce(SUM) of the int64 error
+counters (and MAX of elapsed time) at the end of a run or report window, and -- when
+each rank holds only its own buffers -- one neighbour halo exchange per contiguous range
+(`exchange_halos`, ~35 KB per side for K = 4096): torch.distributed over NCCL on B200s,
 gloo in the CPU tests.
 """
 from __future__ import annotations
@@ -57,3 +58,37 @@ def reduce_counts(local: dict, elapsed_ms: float, device=None, group=None):
     out = {k: int(v[i]) for i, k in enumerate(COUNT_KEYS)}
     out["flags"] = int(v[-1])
     return out, float(t.item())
+
+
+def exchange_halos(stream, left: int, right: int, group=None):
+    """Halo exchange between neighbouring ranks ("the first buffer's left
+    halo and the last buffer's right halo can be P2P-exchanged over NVLink").
+
+    stream: this rank's 1-D int16 tensor laid out as [left halo | own buffers | right halo]
+    (contiguous buffer ranges per rank, `shard_range`).  Rank r's left halo is the last
+    `left` own samples of rank r-1 and its right halo the first `right` own samples of
+    rank r+1; both are exchanged with one batch of point-to-point sends/receives (NCCL
+    over NVLink for CUDA tensors, gloo for CPU tensors).  The outer ranks keep the halos
+    they were given (the stream's guard data).  Each rank needs at least max(left, right)
+    own samples.  In place; returns `stream`."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return stream
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n = stream.numel()
+    own_lo, own_hi = left, n - right
+    if own_hi - own_lo < max(left, right):
+        raise ValueError("each rank needs at least max(left, right) own samples")
+    peer = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    ops = []
+    if rank + 1 < world:
+        ops.append(dist.P2POp(dist.isend, stream[own_hi - left:own_hi].contiguous(), peer(rank + 1), group))
+        ops.append(dist.P2POp(dist.irecv, stream[own_hi:], peer(rank + 1), group))
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, stream[own_lo:own_lo + right].contiguous(), peer(rank - 1), group))
+        ops.append(dist.P2POp(dist.irecv, stream[:own_lo], peer(rank - 1), group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return stream

@@ -69,3 +69,45 @@ def test_gloo_world2_reduction():
         assert tot["flags"] == 1
         assert tmax == 11.0
     assert torch is not None
+
+
+def _halo_worker(rank, world, port, q):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2108_07004_b200.sharding import exchange_halos, shard_range
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    N, nbuf, left, right = 1024, 6, 300, 80
+    rng = np.random.default_rng(5)
+    glob = torch.from_numpy(rng.integers(-2048, 2048, left + nbuf * N + right).astype(np.int16))
+    lo, hi = shard_range(nbuf, world, rank)
+    mine = glob[lo * N: hi * N + left + right].clone()  # [left | own | right] window of the global stream
+    want = mine.clone()
+    if rank > 0:
+        mine[:left] = 0          # halos that live on the neighbours
+    if rank + 1 < world:
+        mine[-right:] = 0
+    exchange_halos(mine, left, right)
+    q.put((rank, bool(torch.equal(mine, want))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_halo_exchange(world):
+    """exchange_halos fills every inner rank boundary with the neighbours' samples
+    (SURVEY 8(e) optional P2P halo exchange), world sizes 2 and 3 over gloo."""
+    pytest.importorskip("torch")
+    import torch.multiprocessing as tmp
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res
