@@ -1,6 +1,6 @@
-"""Multi-process (world_size 2, gloo, CPU) tests of the sharding / reduction
-logic used by bench.py under torchrun.  The GPU data path has no collective;
-these cover the host-side plumbing."""
+"""Multi-process (world_size 2-3, gloo, CPU) tests of the sharding / reduction / halo
+exchange logic used by bench.py under torchrun and by multi-rank
+deployments holding per-rank buffer ranges.  The same code runs over NCCL on B200s."""
 import os
 import socket
 
