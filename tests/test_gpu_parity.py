@@ -670,3 +670,40 @@ def test_cspr_hypothesis_sweep():
     rx.close()
     ref.close()
     rx1.close()
+
+
+def test_max_size_int64_offsets():
+    """Maximum sizes: one submission of 520 full-size buffers (2.18 G samples, sample offsets
+    beyond 2^31) cycled from a 2-buffer C1 pool.  Outputs depend only on a buffer's window, so
+    buffer 519 equals buffer 1 bit for bit, every buffer of the noiseless C1 stream decodes
+    without errors, and buffer 1 matches the oracle."""
+    _require_gpu()
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    name = "C1"
+    cfg = configs.get(name).link
+    pool = make_pool(cfg, 2)
+    fir = _fir(name)
+    n = cfg.buffer_len
+    n_sym = n // 4
+    nb = 520
+    assert nb * n > 2 ** 31
+    left, right = halo_for(n)
+    stream, off = make_stream(pool, nb, left, right)
+    src = torch.from_numpy(stream).cuda()
+    del stream
+    out = torch.empty(nb * n_sym, dtype=torch.uint8, device="cuda")
+    rx = KKReceiver(cfg.fmt, n, cfg.cspr_db, fir, pool.dc_offset, tone_bin=cfg.tbin, ref_pattern=pool.pattern,
+                    max_batch=nb)
+    rx.submit_batch(src, off, nb, out)
+    counts = rx.sync(as_array=True)
+    assert len(counts) == nb
+    assert int(counts["bit_errors"].sum()) == 0 and int(counts["sym_errors"].sum()) == 0
+    lab1 = out[1 * n_sym:2 * n_sym].cpu().numpy()
+    lab519 = out[519 * n_sym:520 * n_sym].cpu().numpy()
+    assert np.array_equal(lab1, lab519)
+    # buffer 1 against the oracle (window from the 2-buffer stream: same content)
+    st2, off2 = make_stream(pool, 2, left, right)
+    o = _oracle(st2, off2, 1, cfg, pool, fir, left, right)
+    inv = np.argsort(pool.labels)
+    assert np.array_equal(inv[lab1.astype(np.int64)], o["decisions"])
+    rx.close()
