@@ -1,15 +1,23 @@
 // kk_kernels.cu -- sm_100a kernels of the KK receiver hot path.
 //
-//   kk_chain_kernel<APPLY=true>   the whole per-sample chain, fused: S1 front end,
-//       S2 blockwise Hilbert, S3 reconstruction + carrier removal, S4 static EQ
-//       with 4->2 fold and downconversion, S5' fixed-tap WL apply, S6 decision,
-//       S7 demap + count.  Reads int16 codes, writes uint8 labels; E_s and x2
-//       never leave shared memory.
-//   kk_chain_kernel<APPLY=false>  same S1-S4 code, writes x2 to HBM (only the
-//       tails the LMS update pass needs, or everything for debug / L < N/4).
+//   kk_chain_kernel<PREKK>   the whole per-sample chain, fused, one 512-thread CTA per SM
+//       (4 groups x 4 warps): S1 front end, S2 blockwise Hilbert, S3 reconstruction +
+//       carrier removal, S4 static EQ with 4->2 fold and downconversion, S5' fixed-tap WL
+//       apply, S6 decision, S7 demap + count.  Reads int16 codes, writes uint8 labels;
+//       E_s and x2 never leave shared memory.  Segment modes: APPLY (labels), X2_TAIL (the
+//       x2 tails the next batch's LMS pass reads), X2_FULL (debug / sub_block < N/4).
+//       PREKK = the optional pre-KK intensity FIR fused into the S1/S3 code reads.  The
+//       last CTAs of a streaming launch run the next batch's S5 update pass
+//       (lms_lanes_body: lane per chain, or lms_warp_cta: warp per chain for few chains)
+//       and then join the chain work.
 //   kk_lms_kernel    S5 update pass: one warp per sub-block chain of K steps
 //                    (sequential, "significant time", few resources)
+//   kk_lms_lanes_kernel  the same pass with one lane per chain (one SM for a batch)
 //   kk_apply_kernel  S5'-S7 from materialised x2 (sub_block < buffer only)
+//   kk_unpack12_kernel   packed 12-bit ADC bytes -> int16 codes (host-input path)
+//   kk_gram_kernel / kk_chol_solve_kernel   init-time LS fit of the static EQ (fp64)
+//   kk_fsync_kernel  init-time frame synchronisation against the PCG64 pattern
+//   kk_gmi_kernel    batched AWGN GMI of constellations (GS optimiser workload)
 //
 // No tensor cores: nothing here is a dense contraction.
 #include <cuda_runtime.h>
