@@ -914,23 +914,22 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           const int lim = (int)((a.N - sbase < (int64_t)(1 << 30)) ? a.N - sbase : (int64_t)(1 << 30)) - e_off;
           unsigned clip = 0;
           float cmin = __int_as_float(0x7f800000);
-          // phi to the imaginary slot of its own output (same lane writes and later reads it),
+          // both phases of window position m (chunk c0: v.x; chunk c0 + 1: -v.y) as one float2
+          // in output slot m (the same lane writes and later reads it; 64-bit, conflict-free),
           // then one rolled loop over the 32 outputs (keeps the kernel's code small)
 #pragma unroll
-          for (int n2 = 8; n2 < 24; ++n2) {
-            dst[lane + 32 * n2].y = v[n2].x;
-            dst[lane + 32 * n2 + 512].y = -v[n2].y;
-          }
+          for (int n2 = 8; n2 < 24; ++n2) dst[lane + 32 * n2] = v[n2];
           // outputs mm = lane + 256 + 32 t (chunk c0) and mm + 512 (chunk c0 + 1), t = 0..15
           const int16_t* sp0 = src + PKH + s_off + lane + 256;
           float2* dp0 = dst + lane + 256;
           const bool allin = lim >= 1280;  // every output position of this task is < N
 #pragma unroll 2
           for (int t = 0; t < 16; ++t) {
+            const float2 ph = dp0[32 * t];  // read before output slot m is overwritten below
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               const int o = 32 * t + 512 * hh;
-              const float phi = dp0[o].y;
+              const float phi = hh ? -ph.y : ph.x;
               const float cv = !PREKK ? (float)sp0[o] + sg.dc
                                : (!warm ? reinterpret_cast<const float*>(xs)[1024 * warp + 32 * (t + 16 * hh) + lane]
                                         : prek_v<true>(a, sp0, o, sg));
