@@ -707,3 +707,49 @@ def test_max_size_int64_offsets():
     inv = np.argsort(pool.labels)
     assert np.array_equal(inv[lab1.astype(np.int64)], o["decisions"])
     rx.close()
+
+
+def test_totals_timing_and_cspr_setter():
+    """Bookkeeping calls of the C ABI: kk_rx_totals accumulates exactly the per-buffer
+    counters of process_batch and the streaming pipeline, kk_rx_reset_totals clears them;
+    kk_rx_set_cspr on a handle gives bit for bit what a handle created with that CSPR gives;
+    kk_rx_set_timing / kk_rx_kernel_times report a positive chain time; kk_rx_last_launches
+    counts the kernels of the last synchronous call."""
+    _require_gpu()
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    name = "C2_n16"
+    cfg = configs.get(name).link
+    pool = make_pool(cfg, 3)
+    fir = _fir(name)
+    n = cfg.buffer_len
+    left, right = halo_for(n)
+    stream, off = make_stream(pool, 3, left, right)
+    src = torch.from_numpy(stream).cuda()
+    kw = dict(tone_bin=cfg.tbin, ref_pattern=pool.pattern, max_batch=3)
+    rx = KKReceiver(cfg.fmt, n, cfg.cspr_db, fir, pool.dc_offset, **kw)
+    rx.set_timing(True)
+    c = rx.process_batch(src, off, 3)
+    assert rx.last_launches() >= 2
+    t = rx.totals()
+    for k in ("bit_errors", "sym_errors", "bits", "symbols", "clipped_samples", "gated_updates"):
+        assert t[k] == sum(x[k] for x in c), k
+    kt = rx.kernel_times()
+    assert kt["chain"][1] >= 1 and kt["chain"][0] > 0.0
+    rx.reset_totals()
+    assert all(v == 0 for k, v in rx.totals().items() if k != "flags")
+    rx.submit_batch(src, off, 3)
+    cs = rx.sync()
+    assert [x["bit_errors"] for x in cs] == [x["bit_errors"] for x in c]
+    assert rx.totals()["bit_errors"] == sum(x["bit_errors"] for x in c)
+    # CSPR setter == a handle created with that CSPR (A_hat follows, reading R6)
+    c2 = cfg.cspr_db + 2.0
+    rx.set_cspr(c2)
+    out_a = torch.empty(3 * (n // 4), dtype=torch.uint8, device="cuda")
+    ca = rx.process_batch(src, off, 3, out_a)
+    ref = KKReceiver(cfg.fmt, n, c2, fir, pool.dc_offset, **kw)
+    out_b = torch.empty(3 * (n // 4), dtype=torch.uint8, device="cuda")
+    cb = ref.process_batch(src, off, 3, out_b)
+    assert ca == cb
+    assert torch.equal(out_a, out_b)
+    rx.close()
+    ref.close()
