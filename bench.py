@@ -183,6 +183,11 @@ def oracle_rate(name, n_pool, workers, tasks):
 
 
 def run_reference(args):
+    """The reference arm: the float64 oracle (oracle/, as it stands) on the host cores, same
+    workload / metric / unit.  A step is ONE whole C5 buffer (a bounded sample of the
+    workload); the K steps run concurrently on `workers` host processes (spawn and input
+    loading inside the timed region), so value = K buffers x 2^22 samples / wall time and the
+    run ends within a minute or two whatever K is.  Under torchrun only rank 0 runs."""
     rank = _env_int("RANK", 0)
     if rank != 0:
         return 0
@@ -190,23 +195,18 @@ def run_reference(args):
     from synth import configs
     from synth.generate import make_pool
     make_pool(configs.get(args.workload).link, args.pool)  # warm the input cache outside the timed steps
-    for _ in range(args.warmup):
-        oracle_rate(args.workload, args.pool, workers, workers)
-    times, samples = [], 0
-    for _ in range(args.steps):
-        _, dt, s = oracle_rate(args.workload, args.pool, workers, workers)
-        times.append(dt)
-        samples += s
-    total = sum(times)
-    value = samples / total / 1e9
+    oracle_rate(args.workload, args.pool, workers, min(max(args.warmup, 1), workers))  # W untimed buffers
+    value, total, samples = oracle_rate(args.workload, args.pool, workers, args.steps)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload + " (GS-128 CSPR 16 dB two-sided OSNR 35 dB, 2^22-sample buffers)",
-                   "buffers_per_step": workers, "l2": "inputs > L2 not applicable (CPU)"},
+                   "buffers_per_step": 1, "host_processes": workers,
+                   "l2": "inputs > L2 not applicable (CPU)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle",
-                         "sample": f"{workers} whole 2^22-sample buffers per step, one per process"},
+                         "sample": f"{args.steps} whole 2^22-sample buffers (one per step) on {workers} processes "
+                                   f"({total:.1f} s)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
