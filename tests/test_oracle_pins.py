@@ -555,3 +555,56 @@ def test_frame_sync_on_oracle_field():
     k, ck, mean = train.frame_sync(e_s, e_pos0, pool.points, pool.pattern, 64, 1024)
     assert k == s
     assert abs(ck) ** 2 > 20 * mean
+
+
+def test_train_fir_recovers_planted_equaliser():
+    """oracle.train.train_fir (reading R4: the 203-tap FIR at 4 sps,
+    y_n = sum_t h[t] E_s[4n + 101 - t], LS-fitted to the known symbols).  Targets made by
+    np.convolve of the oracle's own S1-S3 field with planted random taps: the unregularised
+    fit returns those taps to 1e-8 (a transposed or shifted tap index cannot), the
+    default-ridge fit reproduces the targets, and a fit one symbol off does not."""
+    from oracle import train
+    from synth.generate import LinkConfig, make_pool, make_stream
+    cfg = LinkConfig("QAM4", 12.0, 7.0, "one_sided", 1 << 15, seed_noise=5)
+    pool = make_pool(cfg, 1, cache=False)
+    st, off = make_stream(pool, 1, 2048, 2048)
+    p = O.RxParams(buffer_len=cfg.buffer_len, cspr_db=cfg.cspr_db, dc_offset=pool.dc_offset,
+                   fir=np.zeros(O.FIR_TAPS), points=pool.points, labels=pool.labels, tone_bin=cfg.tbin)
+    window = st[: off + 4 * 2048 + 2048]
+    e_s, e0 = train.field_after_s3(window, off, p)
+    h = np.array([1.0, 1j]) @ np.random.default_rng(3).standard_normal((2, O.FIR_TAPS))
+    n0, cnt = 40, 1500
+    n = np.arange(n0, n0 + cnt)
+    s = np.convolve(e_s, h)[4 * n + O.FIR_HALF - e0]
+    h0 = train.train_fir(window, off, p, s, n0, cnt, ridge=0.0)
+    assert np.max(np.abs(h0 - h)) <= 1e-8 * np.max(np.abs(h))
+    hd = train.train_fir(window, off, p, s, n0, cnt)
+    yd = np.convolve(e_s, hd)[4 * n + O.FIR_HALF - e0]
+    assert np.linalg.norm(yd - s) <= 1e-6 * np.linalg.norm(s)
+    hs = train.train_fir(window, off, p, s, n0 + 1, cnt)
+    assert np.max(np.abs(hs - h)) > 0.5 * np.max(np.abs(h))
+
+
+def test_gmi_4qam_equals_twice_bpsk_capacity():
+    """oracle.shaping.gmi_awgn (GS points chosen by GMI on the AWGN channel).
+    Gray 4-QAM is two independent BPSK bits, one per dimension, so its GMI is exactly
+    2 C_BPSK(a = 1/sqrt 2, sigma^2/2), with C_BPSK = 1 - E log2(1 + exp(-2 a y / s2)),
+    y ~ N(a, s2).  That integral is done here by adaptive scipy quadrature, independently of
+    the oracle's Gauss-Hermite rule.  The order-40 rule matches to 5e-5 bit; the default
+    order 10 is within 5e-3 (its quadrature error, largest near 5 dB)."""
+    from scipy import integrate
+    from oracle import shaping
+    pts, labs = C.make_standard("QAM4")
+
+    def c_bpsk(a, s2):
+        def f(y):
+            return (np.exp(-(y - a) ** 2 / (2 * s2)) / np.sqrt(2 * np.pi * s2)
+                    * np.logaddexp(0.0, -2 * a * y / s2) / np.log(2))
+        r = 40 * np.sqrt(s2)
+        return 1.0 - integrate.quad(f, a - r, a + r, limit=200, epsabs=1e-13)[0]
+
+    for snr_db in (-5.0, 0.0, 5.0, 10.0, 15.0):
+        ref = 2 * c_bpsk(1 / np.sqrt(2), 10 ** (-snr_db / 10) / 2)
+        assert abs(shaping.gmi_awgn(pts, labs, snr_db, order=40) - ref) <= 5e-5, snr_db
+        assert abs(shaping.gmi_awgn(pts, labs, snr_db) - ref) <= 5e-3, snr_db
+    assert abs(shaping.gmi_awgn(pts, labs, 40.0, order=40) - 2.0) <= 1e-9
