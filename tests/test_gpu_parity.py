@@ -289,6 +289,49 @@ def test_async_pipeline_equals_process_batch():
     ref.close()
 
 
+
+def test_async_update_pass_mode_switch():
+    """Consecutive submissions on either side of the in-launch update-pass switch
+    (LMS_WARP_MAX_CHAINS = 60 in kk_rx.cu: warp-per-chain CTAs at <= 60 buffers, one
+    lane-per-chain CTA above) hand their taps and x2 tails to each other: labels and
+    counters stay bit-identical to one kk_rx_process_batch over all 130 buffers."""
+    _require_gpu()
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    name = "C2_n16"
+    cfg = configs.get(name).link
+    pool = make_pool(cfg, 6)
+    fir = _fir(name)
+    left, right = halo_for(cfg.buffer_len)
+    nbuf = 130
+    stream, off = make_stream(pool, nbuf, left, right)
+    n = cfg.buffer_len
+    n_sym = n // 4
+
+    def rx():
+        return KKReceiver(cfg.fmt, n, cfg.cspr_db, fir, pool.dc_offset, tone_bin=cfg.tbin, ref_pattern=pool.pattern,
+                          max_batch=nbuf)
+    src = torch.from_numpy(stream).cuda()
+    ref = rx()
+    out_ref = torch.empty(nbuf * n_sym, dtype=torch.uint8, device="cuda")
+    c_ref = ref.process_batch(src, off, nbuf, out_ref)
+    lab_ref = out_ref.cpu().numpy()
+    ref.close()
+    r = rx()
+    out = torch.empty(nbuf * n_sym, dtype=torch.uint8, device="cuda")
+    for sizes in ((62, 3, 65), (1, 61, 60, 8)):  # lanes -> warp -> lanes; warp -> lanes -> warp
+        out.zero_()
+        r.seek(0)
+        b0 = 0
+        for k in sizes:
+            r.submit_batch(src, off + b0 * n, k, out[b0 * n_sym:(b0 + k) * n_sym])
+            b0 += k
+        assert b0 == nbuf
+        c = r.sync()
+        torch.cuda.synchronize()
+        assert c == c_ref, sizes
+        assert np.array_equal(out.cpu().numpy(), lab_ref), sizes
+    r.close()
+
 def test_async_full_size_bench_config():
     """The bench's launch configuration: C5 (GS-128) at full size, 128-buffer
     submissions through the async pipeline, device-resident.  Two submissions equal
