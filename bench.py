@@ -389,9 +389,42 @@ def run_gpu(args):
         v_int16 = e2e_run(False)
         span = left + B * N + right
         d2h = B * (N // 4) + B * 64
+
+        # the PCIe ceiling of this leg on this box: one step's packed H2D and symbol D2H as
+        # plain pinned copies on two streams (no kernels), CUDA events, 5 repetitions
+        h_step = h_packed[:span * 3 // 2]
+        d_scr = torch.empty(h_step.numel(), dtype=torch.uint8, device=dev)
+        d_o = torch.zeros(h_out[0].numel(), dtype=torch.uint8, device=dev)
+        cs1, cs2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+        def copies():
+            cs1.wait_stream(cur)
+            cs2.wait_stream(cur)
+            with torch.cuda.stream(cs1):
+                d_scr.copy_(h_step, non_blocking=True)
+            with torch.cuda.stream(cs2):
+                h_out[0].copy_(d_o, non_blocking=True)
+            cur.wait_stream(cs1)
+            cur.wait_stream(cs2)
+
+        copies()
+        torch.cuda.synchronize(dev)
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(cur)
+        for _ in range(5):
+            copies()
+        p1.record(cur)
+        torch.cuda.synchronize(dev)
+        pcie_ms = p0.elapsed_time(p1) / 5
+        del d_scr, d_o
         e2e = {"value": v_packed, "unit": UNIT, "h2d_bytes_per_step": span * 3 // 2, "d2h_bytes_per_step": d2h,
                "input": "packed 12-bit ADC samples (kk_rx_submit_batch_packed12), pinned host memory",
-               "int16_input_value": v_int16, "int16_h2d_bytes_per_step": span * 2}
+               "int16_input_value": v_int16, "int16_h2d_bytes_per_step": span * 2,
+               "pcie_ceiling": {"value": B * N / (pcie_ms / 1e3) / 1e9 * world, "unit": UNIT,
+                                "ms_per_step": pcie_ms, "frac": v_packed / (B * N / (pcie_ms / 1e3) / 1e9 * world),
+                                "basis": "one step's packed H2D + symbol D2H as plain pinned copies on two "
+                                         "streams, no kernels (tools/pcie_bw.py)"}}
 
     if rank != 0:
         rx.close()
