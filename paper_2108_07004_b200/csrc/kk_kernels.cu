@@ -1648,58 +1648,66 @@ __global__ void __launch_bounds__(1024) kk_chol_solve_kernel(double2* __restrict
   __syncthreads();
   for (int k = threadIdx.x; k < n; k += blockDim.x) R[(int64_t)k * n + k].x += ridge * s_tr / n;
   __syncthreads();
-  // Cholesky R = L L^H (lower triangle overwritten)
+  // Cholesky R = L L^H (lower triangle overwritten); column k of L staged in shared memory,
+  // the trailing update one row per warp (j <= i over the lanes)
+  __shared__ double2 s_col[256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   for (int k = 0; k < n; ++k) {
-    if (threadIdx.x == 0) {
-      const double d = sqrt(R[(int64_t)k * n + k].x);
-      R[(int64_t)k * n + k] = make_double2(d, 0.0);
-    }
-    __syncthreads();
-    const double inv = 1.0 / R[(int64_t)k * n + k].x;
+    const double d = sqrt(R[(int64_t)k * n + k].x);
+    const double inv = 1.0 / d;
     for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) {
       double2 v = R[(int64_t)i * n + k];
-      R[(int64_t)i * n + k] = make_double2(v.x * inv, v.y * inv);
+      v = make_double2(v.x * inv, v.y * inv);
+      R[(int64_t)i * n + k] = v;
+      s_col[i] = v;
     }
     __syncthreads();
-    // trailing update R[i][j] -= L[i][k] conj(L[j][k]), j <= i
-    const int m = n - k - 1;
-    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-      const int i = k + 1 + idx / m, j = k + 1 + idx % m;
-      if (j > i) continue;
-      const double2 li = R[(int64_t)i * n + k], lj = R[(int64_t)j * n + k];
-      double2 r = R[(int64_t)i * n + j];
-      r.x -= li.x * lj.x + li.y * lj.y;
-      r.y -= li.y * lj.x - li.x * lj.y;
-      R[(int64_t)i * n + j] = r;
+    if (threadIdx.x == 0) R[(int64_t)k * n + k] = make_double2(d, 0.0);
+    // trailing update R[i][j] -= L[i][k] conj(L[j][k]), k < j <= i
+    for (int i = k + 1 + warp; i < n; i += nwarp) {
+      const double2 li = s_col[i];
+      for (int j = k + 1 + lane; j <= i; j += 32) {
+        const double2 lj = s_col[j];
+        double2 r = R[(int64_t)i * n + j];
+        r.x -= li.x * lj.x + li.y * lj.y;
+        r.y -= li.y * lj.x - li.x * lj.y;
+        R[(int64_t)i * n + j] = r;
+      }
     }
     __syncthreads();
   }
-  // forward L y = b, backward L^H h = y (one thread: n^2 operations)
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < n; ++i) {
-      double2 s = b[i];
-      for (int j = 0; j < i; ++j) {
-        const double2 l = R[(int64_t)i * n + j], y = b[j];
-        s.x -= l.x * y.x - l.y * y.y;
-        s.y -= l.x * y.y + l.y * y.x;
-      }
-      const double d = R[(int64_t)i * n + i].x;
-      b[i] = make_double2(s.x / d, s.y / d);
+  // forward L y = b, backward L^H h = y: column-oriented substitution, the right-hand side
+  // in shared memory, one pivot per step and the n - i remaining updates spread over the CTA
+  __shared__ double2 s_b[256];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_b[i] = b[i];
+  __syncthreads();
+  for (int i = 0; i < n; ++i) {
+    const double d = R[(int64_t)i * n + i].x;
+    const double2 yi = make_double2(s_b[i].x / d, s_b[i].y / d);
+    __syncthreads();
+    if (threadIdx.x == 0) s_b[i] = yi;
+    for (int j = i + 1 + threadIdx.x; j < n; j += blockDim.x) {  // y_j -= L[j][i] y_i
+      const double2 l = R[(int64_t)j * n + i];
+      s_b[j].x -= l.x * yi.x - l.y * yi.y;
+      s_b[j].y -= l.x * yi.y + l.y * yi.x;
     }
-    for (int i = n - 1; i >= 0; --i) {
-      double2 s = b[i];
-      for (int j = i + 1; j < n; ++j) {
-        const double2 l = R[(int64_t)j * n + i], y = b[j];  // conj(L[j][i]) * h_j
-        s.x -= l.x * y.x + l.y * y.y;
-        s.y -= l.x * y.y - l.y * y.x;
-      }
-      const double d = R[(int64_t)i * n + i].x;
-      b[i] = make_double2(s.x / d, s.y / d);
+    __syncthreads();
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    const double d = R[(int64_t)i * n + i].x;
+    const double2 hi = make_double2(s_b[i].x / d, s_b[i].y / d);
+    __syncthreads();
+    if (threadIdx.x == 0) s_b[i] = hi;
+    for (int j = threadIdx.x; j < i; j += blockDim.x) {  // y_j -= conj(L[i][j]) h_i
+      const double2 l = R[(int64_t)i * n + j];
+      s_b[j].x -= l.x * hi.x + l.y * hi.y;
+      s_b[j].y -= l.x * hi.y - l.y * hi.x;
     }
-    for (int i = 0; i < n; ++i) {
-      out[2 * i] = (float)b[i].x;
-      out[2 * i + 1] = (float)b[i].y;
-    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    out[2 * i] = (float)s_b[i].x;
+    out[2 * i + 1] = (float)s_b[i].y;
   }
 }
 
