@@ -61,3 +61,11 @@ def snr_one_sided(osnr_db, cspr_db, baud=1e9, ref_bw=12.5e9):
     N0 * 12.5 GHz = P_total 10^(-OSNR/10), P_total = P_s (1 + c)."""
     c = 10 ** (cspr_db / 10)
     return osnr_db + 10 * math.log10(ref_bw / baud) - 10 * math.log10(1 + c)
+
+
+def snr_two_sided(osnr_db, cspr_db, baud=1e9, ref_bw=12.5e9):
+    """Predicted Es/N0 (dB) after KK detection for the two-sided (physical) noise mode:
+    the ASE is flat on both sides of the tone, so the image-band noise beats with the
+    carrier onto the same baseband frequencies as the signal-band noise and the
+    in-band noise doubles: snr_one_sided - 10 log10(2) (SURVEY.md 8(c) reading 14)."""
+    return snr_one_sided(osnr_db, cspr_db, baud, ref_bw) - 10 * math.log10(2.0)

@@ -33,8 +33,16 @@ def field_after_s3(window, left, p: O.RxParams):
     return e_s, e_pos0
 
 
-def train_fir(window, left, p: O.RxParams, symbols_tx, n_first, n_count, ridge=1e-9):
-    """min_h sum_n |sum_t h[t] E_s[4n + 101 - t] - s_n|^2 + ridge ||h||^2."""
+def train_fir(window, left, p: O.RxParams, symbols_tx, n_first, n_count, ridge=1e-9, unbiased=False):
+    """min_h sum_n |sum_t h[t] E_s[4n + 101 - t] - s_n|^2 + ridge ||h||^2.
+
+    On a noisy training buffer (the live link of PAPER l.53) this least-squares fit is
+    the sample MMSE filter: it also weighs the noise the KK front end folds into the
+    band, so it constrains the stopband a noiseless fit leaves free.  The MMSE
+    estimate is biased toward zero, x = g s + noise with g = <x, s>/<s, s> < 1, which
+    shrinks the constellation against the fixed decision regions (S6); unbiased=True
+    returns h / g (the unbiased MMSE filter, same SNR, unit gain on the training
+    symbols).  DESIGN.md reading R4."""
     e_s, e_pos0 = field_after_s3(window, left, p)
     n = np.arange(n_first, n_first + n_count, dtype=np.int64)
     t = np.arange(O.FIR_TAPS, dtype=np.int64)
@@ -44,6 +52,10 @@ def train_fir(window, left, p: O.RxParams, symbols_tx, n_first, n_count, ridge=1
     AhA = A.conj().T @ A
     AhA += ridge * np.trace(AhA).real / O.FIR_TAPS * np.eye(O.FIR_TAPS)
     h = np.linalg.solve(AhA, A.conj().T @ b)
+    if unbiased:
+        x = A @ h
+        g = np.vdot(b, x) / np.vdot(b, b)
+        h = h / g
     return h
 
 

@@ -608,3 +608,90 @@ def test_gmi_4qam_equals_twice_bpsk_capacity():
         assert abs(shaping.gmi_awgn(pts, labs, snr_db, order=40) - ref) <= 5e-5, snr_db
         assert abs(shaping.gmi_awgn(pts, labs, snr_db) - ref) <= 5e-3, snr_db
     assert abs(shaping.gmi_awgn(pts, labs, 40.0, order=40) - 2.0) <= 1e-9
+
+
+# ------------------------------------------------------------- carrier amplitude (A.3)
+def test_carrier_amplitude_equals_generator_tone():
+    """Reading R6 / SURVEY A.3: on a noiseless generated buffer the static carrier
+    estimate A_hat = sqrt(d c / (1 + c)) equals the tone the GENERATOR put in, scaled by
+    its ADC gain, sqrt(g) * A with A = sqrt(c) (synth.generate._tone): d = g mean(I) and
+    mean(I) = 1 + c exactly (unit-power signal, tone on a bin outside the signal band).
+    Independently of that formula, the field the chain reconstructs in the tone frame,
+    E' = a e^{i phi} (S1 + S2, before the carrier subtraction of S3), has its mean at the
+    same sqrt(g) A (the tone is the only DC component of E')."""
+    from synth import configs
+    from synth.generate import make_pool
+    for name in ("C1_n16", "C4_n16"):
+        cfg = configs.get(name).link
+        pool = make_pool(cfg, 1, cache=False, noiseless=True)
+        c = 10 ** (cfg.cspr_db / 10)
+        a_gen = math.sqrt(pool.gain) * math.sqrt(c)
+        a_hat = O.carrier_amplitude(pool.dc_offset, cfg.cspr_db)
+        assert abs(a_hat - a_gen) <= 1e-6 * a_gen, (a_hat, a_gen)   # d is float32
+        codes = pool.codes[0]
+        n = len(codes)
+        win = np.concatenate([codes[-256:], codes, codes[:256]])    # circular halo (periodic buffer)
+        a, l, _ = O.frontend(win, pool.dc_offset, 1.0)
+        phi = O.hilbert_phase(l, -256, 0, n // 512 - 1)
+        e_tf = a[256:256 + n] * np.exp(1j * phi)
+        m = np.mean(e_tf)
+        assert abs(abs(m) - a_gen) <= 2e-4 * a_gen, (abs(m), a_gen)
+        assert abs(np.angle(m)) <= 2e-4
+        # the wrong CSPR in the formula is visible: 1 dB off moves A_hat by > 0.1 % (>> 1e-6)
+        assert abs(O.carrier_amplitude(pool.dc_offset, cfg.cspr_db + 1.0) - a_gen) > 1e-3 * a_gen
+
+
+# ------------------------------------------------------------- LMS fixed point (Wiener)
+def test_lms_converges_to_wiener_gain():
+    """LMS with a known reference (PILOT, the paper's training mode) is a
+    stochastic-gradient solver of the Wiener (MMSE) equations: for x2 = s + n at the
+    symbol instants (white complex noise, Es/N0 = SNR) and independent noise at the half
+    instants, the Wiener taps are w = (0, SNR/(1+SNR), 0, 0), g = 0.  The decision-
+    directed soft-gated mode (the default, DD_SOFT) reaches the same fixed point when
+    decisions are reliable (4-QAM at 12 dB).  This gain bias is what makes the adaptive
+    stage shrink the constellation (C2 BER note)."""
+    pts, labs = C.make_standard("QAM4")
+    rng = np.random.default_rng(12)
+    n_sym = 200000
+    snr = 10 ** 1.2
+    pat = rng.integers(0, 4, n_sym)
+    s = pts[pat]
+    sig = math.sqrt(1 / snr / 2)
+    x2 = np.empty(2 * n_sym + 4, dtype=np.complex128)
+    x2[0::2] = sig * (rng.standard_normal(n_sym + 2) + 1j * rng.standard_normal(n_sym + 2))
+    x2[2::2][:n_sym] += s                      # x2_at(2n) = x2[2n + 2] carries s_n (centre tap, index 1)
+    x2[1::2] = sig * (rng.standard_normal(n_sym + 2) + 1j * rng.standard_normal(n_sym + 2))
+    x2_at = lambda m: x2[m + 2]  # noqa: E731
+    wiener = snr / (1 + snr)
+    tau = O.d_min(pts) ** 2 / 4
+    for mode, t in ((O.UPD_PILOT, 0.0), (O.UPD_DD_SOFT, tau)):
+        w, g, _, _ = O.wl_lms_update(x2_at, 0, n_sym - 2, [0, 1, 0, 0], [0] * 4, 2e-4, pts, t, mode, pat, 0)
+        assert abs(w[1] - wiener) <= 6e-3, (mode, w)
+        assert np.max(np.abs(np.r_[w[[0, 2, 3]], g])) <= 6e-3, (mode, w, g)
+
+
+# ------------------------------------------------------------- GS optimiser
+def test_optimize_recovers_gray_4qam():
+    """PAPER l.124 optimiser (oracle.shaping.optimize): started from 4-QAM with a
+    non-Gray labelling (diagonal points differ in one bit), the label swaps must find a
+    Gray labelling (every pair of nearest neighbours differs in exactly one bit) and the
+    GMI must reach Gray 4-QAM's, which is pinned to 2 C_BPSK by independent quadrature
+    (test_gmi_4qam_equals_twice_bpsk_capacity); the accepted-GMI trace never decreases."""
+    from oracle import shaping
+    pts, labs = C.make_standard("QAM4")
+    order = np.argsort(np.angle(pts))          # the 4 points counter-clockwise
+    bad = np.empty(4, dtype=np.int64)
+    bad[order] = [0, 1, 2, 3]                  # natural binary around the square: 1-2 and 3-0 differ in 2 bits
+    snr_db = 5.0
+    g_gray = shaping.gmi_awgn(pts, labs, snr_db, order=20)
+    g_bad = shaping.gmi_awgn(pts, bad, snr_db, order=20)
+    assert g_bad < g_gray - 0.05
+    p2, l2, trace = shaping.optimize(pts, bad, snr_db, iters=60, seed=3, order=20)
+    assert np.all(np.diff(trace) >= 0)
+    d = np.abs(p2[:, None] - p2[None, :]) + np.eye(4) * 9
+    for k in range(4):
+        near = np.argsort(d[k])[:2]
+        for j in near:
+            assert bin(int(l2[k]) ^ int(l2[j])).count("1") == 1, (l2, k, j)
+    assert trace[-1] >= g_gray - 1e-3      # (accepted point moves made before the swap leave a near-square geometry)
+    assert trace[-1] <= g_gray + 2e-3   # point moves cannot beat Gray QPSK by more than the quadrature error
