@@ -45,6 +45,18 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 FP32_MEASURED_TFLOPS = 7.652 * 32 * 2 * 148 / 1e3  # tools/microbench/f32x2_rate.cu, 32 warps/SM
 
 
+def cpu_model():
+    """The host CPU model (lscpu "Model name"), stated beside the cpu_baseline core count."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.lower().startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def _env_int(k, d):
     try:
         return int(os.environ.get(k, d))
@@ -204,7 +216,7 @@ def run_reference(args):
         "config": {"workload": args.workload + " (GS-128 CSPR 16 dB two-sided OSNR 35 dB, 2^22-sample buffers)",
                    "buffers_per_step": 1, "host_processes": workers,
                    "l2": "inputs > L2 not applicable (CPU)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle", "cpu_model": cpu_model(),
                          "sample": f"{args.steps} whole 2^22-sample buffers (one per step) on {workers} processes "
                                    f"({total:.1f} s)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -223,20 +235,26 @@ def run_gpu(args):
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        print(f"[bench] rank {rank}/{world} local {local}: process group backend {dist.get_backend()}, "
+              f"world {dist.get_world_size()}", file=sys.stderr, flush=True)
     dev = torch.device("cuda", local)
 
     from paper_2108_07004_b200 import KKReceiver, halo_for
     from synth import configs
     from synth.generate import make_pool, make_stream
 
+    from paper_2108_07004_b200.sharding import comm_info, max_over_ranks, rank_batches, reduce_counts, shard_range, \
+        sum_counts
+
     wl = configs.get(args.workload)
     cfg = wl.link
     N = cfg.buffer_len
     B = args.batch
     P = args.pool
+    S = args.stream or wl.n_buffers  # C5: the continuous 4096-buffer stream, sharded contiguously over the ranks
     # rank 0 generates (and caches) the pool first, then the others load it
     if rank == 0:
         pool = make_pool(cfg, P)
@@ -250,22 +268,27 @@ def run_gpu(args):
     span = P + B
     stream_np, off = make_stream(pool, span, left, right, first=0)
     d_stream = torch.from_numpy(stream_np).to(dev)
-    d_out = [torch.empty(B * (N // 4), dtype=torch.uint8, device=dev) for _ in range(2)]
+    d_out = [torch.empty(B * (N // 4), dtype=torch.uint8, device=dev) for _ in range(3)]
     cur = torch.cuda.current_stream(dev)
     rx = KKReceiver("CUSTOM" if not cfg.fmt.startswith("QAM") else cfg.fmt, N, cfg.cspr_db, fir, pool.dc_offset,
                     points=pool.points, labels=pool.labels, tone_bin=cfg.tbin, ref_pattern=pool.pattern,
                     device=local, stream=cur.cuda_stream, max_batch=B)
 
-    def first_buf(step):
-        # weak scaling: rank r walks the pool from its own offset
-        return (rank * B + step * B * world) % P
+    def batches(step):
+        # this rank's batches of stream buffers in `step`: the S-buffer stream is sharded into
+        # contiguous per-rank ranges (sharding.rank_batches; stream buffer b = pool buffer b % P,
+        # whose window starts at off + (b % P) N in the cycled device layout)
+        return rank_batches(step, rank, world, B, S, args.scaling)
 
-    # the streaming receiver: kk_rx_submit_batch per step (the LMS update pass of batch
+    nsub = [0]
+
+    # the streaming receiver: kk_rx_submit_batch per batch (the LMS update pass of batch
     # j overlaps the fused chain of batch j-1), kk_rx_sync once after the last step
     def submit_dev(s):
-        b0 = first_buf(s)
-        rx.seek(b0)
-        rx.submit_batch(d_stream, off + b0 * N, B, d_out[s & 1])
+        for b0, cnt in batches(s):
+            rx.seek(b0)
+            rx.submit_batch(d_stream, off + (b0 % P) * N, cnt, d_out[nsub[0] % 3][: cnt * (N // 4)])
+            nsub[0] += 1
 
     for s in range(args.warmup):
         submit_dev(s)
@@ -288,15 +311,16 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1)
+    local = sum_counts(counts)
     launches = rx.async_launches()
     ktimes = rx.kernel_times()
     rx.set_timing(False)
 
     # the same steps through the synchronous call (one batch at a time, LMS pass not hidden)
     def step_sync(s):
-        b0 = first_buf(s)
-        rx.seek(b0)
-        return rx.process_batch(d_stream, off + b0 * N, B, d_out[0], as_array=True)
+        for b0, cnt in batches(s):
+            rx.seek(b0)
+            rx.process_batch(d_stream, off + (b0 % P) * N, cnt, d_out[0][: cnt * (N // 4)], as_array=True)
     step_sync(0)
     torch.cuda.synchronize(dev)
     s0 = torch.cuda.Event(enable_timing=True)
@@ -306,16 +330,10 @@ def run_gpu(args):
         step_sync(s)
     s1.record(cur)
     torch.cuda.synchronize(dev)
-    sync_ms = s0.elapsed_time(s1)
-    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
-    agg = torch.tensor([int(counts["bit_errors"].sum()), int(counts["bits"].sum()),
-                        int(counts["sym_errors"].sum()), int(counts["symbols"].sum())],
-                       dtype=torch.int64, device=dev)
-    if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        dist.all_reduce(agg, op=dist.ReduceOp.SUM)
-    ms_max = float(tmax.item())
-    samples_total = world * args.steps * B * N
+    sync_ms = max_over_ranks(s0.elapsed_time(s1), device=dev)
+    # S8: the only data-path collective -- all_reduce(SUM) of the error counters, MAX of the time
+    tot, ms_max = reduce_counts(local, ms, device=dev)
+    samples_total = tot["symbols"] * 4  # every buffer the ranks processed in the timed steps (4 sps)
     value = samples_total / (ms_max / 1e3) / 1e9
 
     # ---------------- cuFFT comparison (north star: "cuFFT reported only as a comparison";
@@ -327,14 +345,15 @@ def run_gpu(args):
         from paper_2108_07004_b200.cufft_cmp import CufftS1S4
         cm = CufftS1S4(N, B, pool.dc_offset, cfg.cspr_db, fir, tone_bin=cfg.tbin)
         x2_out = torch.empty(B * (N // 2), dtype=torch.complex64, device=dev)
+        cm_first = [batches(s)[0][0] % P for s in range(max(args.warmup, args.steps))]
         for s in range(args.warmup):
-            cm.x2(d_stream, off + first_buf(s) * N, B, x2_out, cur.cuda_stream)
+            cm.x2(d_stream, off + cm_first[s] * N, B, x2_out, cur.cuda_stream)
         torch.cuda.synchronize(dev)
         c0 = torch.cuda.Event(enable_timing=True)
         c1 = torch.cuda.Event(enable_timing=True)
         c0.record(cur)
         for s in range(args.steps):
-            cm.x2(d_stream, off + first_buf(s) * N, B, x2_out, cur.cuda_stream)
+            cm.x2(d_stream, off + cm_first[s] * N, B, x2_out, cur.cuda_stream)
         c1.record(cur)
         torch.cuda.synchronize(dev)
         cms = c0.elapsed_time(c1)
@@ -355,15 +374,17 @@ def run_gpu(args):
         from synth.generate import pack12
         h_packed = torch.from_numpy(pack12(stream_np)).pin_memory()
         h_stream = torch.from_numpy(stream_np).pin_memory()
-        h_out = [torch.empty(B * (N // 4), dtype=torch.uint8).pin_memory() for _ in range(2)]
+        h_out = [torch.empty(B * (N // 4), dtype=torch.uint8).pin_memory() for _ in range(3)]
 
         def submit_host(s, packed):
-            b0 = first_buf(s)
-            rx.seek(b0)
-            if packed:
-                rx.submit_batch_packed12(h_packed, off + b0 * N, B, h_out[s & 1])
-            else:
-                rx.submit_batch(h_stream, off + b0 * N, B, h_out[s & 1])
+            for b0, cnt in batches(s):
+                rx.seek(b0)
+                o = h_out[nsub[0] % 3][: cnt * (N // 4)]
+                nsub[0] += 1
+                if packed:
+                    rx.submit_batch_packed12(h_packed, off + (b0 % P) * N, cnt, o)
+                else:
+                    rx.submit_batch(h_stream, off + (b0 % P) * N, cnt, o)
 
         def e2e_run(packed):
             for s in range(args.warmup):  # W untimed steps (every pipeline slot and its staging)
@@ -380,10 +401,7 @@ def run_gpu(args):
             rx.sync(as_array=True)
             e1.record(cur)
             torch.cuda.synchronize(dev)
-            et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(et, op=dist.ReduceOp.MAX)
-            return samples_total / (float(et.item()) / 1e3) / 1e9
+            return samples_total / (max_over_ranks(e0.elapsed_time(e1), device=dev) / 1e3) / 1e9
 
         v_packed = e2e_run(True)
         v_int16 = e2e_run(False)
@@ -444,15 +462,21 @@ def run_gpu(args):
     lms_avg = ktimes["lms"][0] / max(ktimes["lms"][1], 1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.workload}: GS-128, CSPR 16 dB, two-sided ASE at OSNR 35 dB, "
-                               f"2^22-sample 12-bit buffers, {B} buffers/step/GPU, pool of {P} distinct buffers "
-                               f"cycled (inputs > L2 per step)",
+                               f"2^22-sample 12-bit buffers; a continuous {S}-buffer stream (pool of {P} distinct "
+                               f"buffers cycled) sharded contiguously over {world} GPU(s); "
+                               + (f"{B} buffers/step/GPU walking each rank's own range" if args.scaling == "weak"
+                                  else f"a step = the whole stream, {B}-buffer batches") + " (inputs > L2 per step)",
                    "buffer_len": N, "buffers_per_step_per_gpu": B, "parallelism": f"buffer-sharded x{world}",
+                   "stream_buffers": S, "pool": P,
+                   "shards": [list(shard_range(S, world, r)) for r in range(world)],
+                   "buffers_timed": tot["symbols"] // (N // 4)},
+        "comm": comm_info(),
                    "l2": "inputs larger than L2: each step reads %d x %.0f MiB = %.0f MiB of int16 codes from "
                          "distinct device memory (the %d-buffer pool laid out cycled into a %d-buffer stream); "
-                         "L2 is 126 MB" % (B, N * 2 / 2**20, B * N * 2 / 2**20, P, P + B)},
+                         "L2 is 126 MB" % (B, N * 2 / 2**20, B * N * 2 / 2**20, P, P + B),
         "gbaud_equiv": value / 4.0,
         "hbm_fraction": value * HBM_BYTES_PER_SA / hbm,
         "fp32_fraction_chain": value * FLOP_PER_SA_CHAIN / (FP32_PEAK_TFLOPS * 1e3),
@@ -475,7 +499,8 @@ def run_gpu(args):
                      "lane-per-chain) overlaps the fused chain of batch j-1, whose launch also computes batch j's "
                      "update-pass x2 tails first"),
         "sync_value": samples_total / world / (sync_ms / 1e3) / 1e9 * world,
-        "errors": {"bit_errors": int(agg[0]), "bits": int(agg[1]), "ber": int(agg[0]) / max(int(agg[1]), 1)},
+        "errors": {"bit_errors": tot["bit_errors"], "bits": tot["bits"], "ber": tot["bit_errors"] / max(tot["bits"], 1),
+                   "reduced_over_ranks": "sharding.reduce_counts (all_reduce SUM over the process group)"},
         # context only (north star): the paper's receiver ran the chain in real time at 4 GSa/s
         # (1 GBaud, 4 sps, 12-bit 4 GS/s ADC) on one commercial GPU "with 5120 processing cores"
         # that it "almost fully utilizes"; another machine's number
@@ -492,7 +517,7 @@ def run_gpu(args):
     if world == 1 and not args.no_cpu_baseline:
         workers = args.ref_workers or (os.cpu_count() or 1)
         v, dt, s = oracle_rate(args.workload, P, workers, workers)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": workers, "kind": "oracle",
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": workers, "kind": "oracle", "cpu_model": cpu_model(),
                                 "sample": f"{workers} whole 2^22-sample C5 buffers, one per process ({dt:.1f} s)"}
     print(json.dumps(line), flush=True)
     rx.close()
@@ -509,7 +534,10 @@ def main():
     ap.add_argument("--impl", default="kk", choices=["kk", "reference"])
     ap.add_argument("--workload", default="C5")
     ap.add_argument("--batch", type=int, default=128)
-    ap.add_argument("--pool", type=int, default=16)
+    ap.add_argument("--pool", type=int, default=64, help="distinct buffers of the cycled pool (C5: 64)")
+    ap.add_argument("--stream", type=int, default=0, help="stream length in buffers (0 = the workload's: C5 4096)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: B buffers per GPU per step; strong: a step = the whole stream over all GPUs")
     ap.add_argument("--ref-workers", type=int, default=0, help="oracle processes (0 = all host cores)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

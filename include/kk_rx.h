@@ -187,9 +187,11 @@ kk_status kk_rx_set_dc_offset(kk_rx_t *h, float dc_offset);
  * kk_rx_submit_batch) are processed once per offset dc_values[0..nd-1] (each a full S1-S7
  * pass, back to back through the streaming pipeline; labels are not returned).
  * out_per_dc: nd host structs (counters summed over the buffers) or NULL; *best: index of
- * the lowest bit-error ratio (first on ties).  Drains pending submissions first; restores
- * the handle's DC offset and advances the stream position by nbuf.  KK_EINVAL for bad
- * arguments or non-positive offsets. */
+ * the lowest bit-error ratio (first on ties).  KK_ESTATE while submitted batches are not
+ * yet synced (kk_rx_sync first: their counters are the caller's).  The hypothesis passes
+ * do not count as traffic: kk_rx_totals is unchanged by the call.  Restores the handle's DC
+ * offset and advances the stream position by nbuf.  KK_EINVAL for bad arguments or
+ * non-positive offsets. */
 kk_status kk_rx_dc_sweep(kk_rx_t *h, const int16_t *first, int64_t nbuf, const float *dc_values, int nd,
                          kk_rx_counts *out_per_dc, int *best);
 

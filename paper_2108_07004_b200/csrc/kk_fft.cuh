@@ -102,6 +102,61 @@ __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
 #endif
 __device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
 
+// ---------------------------------------------------------------------------
+// Per-lane tables in tensor memory (TMEM).  Every table the transforms read per lane --
+// the 1024-point twiddles W^(lane r), the 512-point twiddles and the static-EQ spectrum
+// H[lane + 32 k] -- depends only on the lane index, so each thread can hold its own copy in
+// its TMEM lane (tcgen05.ld 32x32b: thread t of a warp reads TMEM lane 32 (warp % 4) + t).
+// That moves ~0.33 shared-memory wavefronts per ADC sample (22 % of the kernel's shared
+// traffic) onto the TMEM read path, which nothing else in this kernel uses (no tensor-core
+// work: DESIGN.md "No tensor cores").  -DKK_TMEM_TABLES=0 restores the shared-memory tables.
+#ifndef KK_TMEM_TABLES
+#define KK_TMEM_TABLES 1
+#endif
+constexpr int TM_TW1024 = 0;   // columns 2(r-1), 2(r-1)+1: W1024^(lane r), r = 1..31 (+2 pad columns)
+constexpr int TM_TW512 = 64;   // W512^(lane r), r = 1..15 (+2 pad)
+constexpr int TM_H = 96;       // H[lane + 32 k], k = 0..31
+constexpr int TM_NCOLS = 160;
+constexpr int TM_ALLOC = 256;  // allocation: power of two >= TM_NCOLS
+
+// 4 complex values (8 TMEM columns) of this thread's lane; asynchronous until tm_wait
+__device__ __forceinline__ void tm_ld4(uint32_t taddr, float2 (&t)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(t[0].x), "=f"(t[0].y), "=f"(t[1].x), "=f"(t[1].y), "=f"(t[2].x), "=f"(t[2].y), "=f"(t[3].x),
+                 "=f"(t[3].y)
+               : "r"(taddr));
+}
+// completes every earlier tm_ld4 of this thread; t = the registers of the one to be used next
+// (tied so no use of them can be scheduled before the wait)
+__device__ __forceinline__ void tm_wait(float2 (&t)[4]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(t[0].x), "+f"(t[0].y), "+f"(t[1].x), "+f"(t[1].y), "+f"(t[2].x), "+f"(t[2].y), "+f"(t[3].x),
+                 "+f"(t[3].y)::"memory");
+}
+__device__ __forceinline__ void tm_st2(uint32_t taddr, float2 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// v[r] *= table[r] for r = R0 .. R0 + 4 NCH - 1 (r < NR), table columns col0 + 2 (r - R0), chunks of 4
+// pipelined one ahead (TMEM load latency ~12 cycles)
+template <int N, int R0, int NR, int NCH>
+__device__ __forceinline__ void tm_twiddle(float2 (&v)[N], uint32_t taddr) {
+  float2 t[2][4];
+  tm_ld4(taddr, t[0]);
+  tm_wait(t[0]);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (c + 1 < NCH) tm_ld4(taddr + 8 * (c + 1), t[(c + 1) & 1]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = R0 + 4 * c + j;
+      if (r < NR) v[r] = c_mul(v[r], t[c & 1][j]);
+    }
+    if (c + 1 < NCH) tm_wait(t[(c + 1) & 1]);
+  }
+}
+
 // a * exp(-2*pi*i*m/32) (used outside the butterflies)
 __device__ __forceinline__ float2 tw32(float2 a, int m) {
   m &= 31;
@@ -205,14 +260,19 @@ __device__ __forceinline__ void dft_brin(float2 (&v)[N]) {
 //   X[k] = sum_n x[n] e^{-2 pi i n k / 1024}
 // scr: this warp's 32 x 33 float tile (wide: 32 x 32 float2); tw: shared table tw[r*32 + l] = e^{-2 pi i r l / 1024}.
 // One copy of the 32-point DFT: the two passes are a loop.
+// tm: this warp's TMEM table address (lane quarter, column 0) when KK_TMEM_TABLES
 __device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __restrict__ scr,
-                                        const float2* __restrict__ tw, bool wide) {
+                                        const float2* __restrict__ tw, uint32_t tm, bool wide) {
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
     dft_brin<32>(v);
     if (pass == 0) {
 #pragma unroll
+#if KK_TMEM_TABLES
+      tm_twiddle<32, 1, 32, 8>(v, tm + TM_TW1024);
+#else
       for (int r = 1; r < 32; ++r) v[r] = c_mul(v[r], tw[r * 32 + lane]);
+#endif
       if (wide) {
         // 64-bit transpose through a 32 x 32 float2 tile (needs 1024 float2 of scratch),
         // columns XOR-swizzled by the row: both directions run at the 2-wavefront minimum
@@ -248,14 +308,18 @@ __device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __rest
 // scr: this warp's tile (>= 16 x 34 floats); tw512[r1*32 + l] = e^{-2 pi i r1 l / 512} (shared).
 // The inverse transform the method needs is conj(DFT(conj(Z))), done by the caller.
 __device__ __forceinline__ void fft512_pairs(float2 (&z)[16], int lane, float* __restrict__ scr,
-                                             const float2* __restrict__ tw512) {
+                                             const float2* __restrict__ tw512, uint32_t tm) {
   const int h = lane & 1, r1 = lane >> 1;
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
     dft_brin<16>(z);
     if (pass == 0) {
 #pragma unroll
+#if KK_TMEM_TABLES
+      tm_twiddle<16, 1, 16, 4>(z, tm + TM_TW512);
+#else
       for (int r = 1; r < 16; ++r) z[r] = c_mul(z[r], tw512[r * 32 + lane]);
+#endif
 #pragma unroll
       for (int r = 0; r < 16; ++r) scr[r * 34 + lane] = z[r].x;
       __syncwarp();

@@ -649,7 +649,39 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     mbar_init(pbar, 1);
     mbar_fence_init();
   }
+#if KK_TMEM_TABLES
+  // per-lane tables in TMEM (kk_fft.cuh): warp 0 allocates; warps 0-3 fill their lane quarter
+  // (every quarter holds the same 32-lane tables, so any warp reads quarter warp % 4)
+  __shared__ uint32_t s_tmem;
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "n"(TM_ALLOC)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem + ((uint32_t)(32 * ((threadIdx.x >> 5) & 3)) << 16);
+  if (threadIdx.x < 128) {
+    const int l = threadIdx.x & 31;
+#pragma unroll 1
+    for (int r = 1; r < 32; ++r) tm_st2(tmem + TM_TW1024 + 2 * (r - 1), a.tw1024[r * 32 + l]);
+    tm_st2(tmem + TM_TW1024 + 62, make_float2(0.f, 0.f));
+#pragma unroll 1
+    for (int r = 1; r < 16; ++r) tm_st2(tmem + TM_TW512 + 2 * (r - 1), a.tw512[r * 32 + l]);
+    tm_st2(tmem + TM_TW512 + 30, make_float2(0.f, 0.f));
+#pragma unroll 1
+    for (int k = 0; k < 32; ++k) tm_st2(tmem + TM_H + 2 * k, a.Hs[l + 32 * k]);
+    tm_wait_st();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#else
+  const uint32_t tmem = 0;
+  __syncthreads();
+#endif
 
   // task role of this warp inside its group, rotated by the group index: warp w of the
   // CTA issues on sub-partition w % 4 and phase H leaves one role idle, so without the
@@ -881,7 +913,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
 #pragma unroll 1
         for (int f = 0; f < nfft; ++f) {
           // H tasks: 64-bit transposes through their own 1024-sample output slice
-          fft1024(v, lane, scr, s_tw, !wt);
+          fft1024(v, lane, scr, s_tw, tmem, !wt);
           if (isH && f == 0) {
             // S2: phi = -H{l} <-> +i sgn(k) L_k (reading R1; the /1024 is in S1), conjugated so the
             // next forward FFT computes the inverse: IFFT(Y) = conj(FFT(conj(Y)))
@@ -984,17 +1016,33 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           // behind the LTI filter: Hs is the DFT of h_i e^{-2 pi i tb i / N}, reading R5)
           const int q = warp;
           float2 z[16];
+#if KK_TMEM_TABLES
+          // H[lane + 32 k2] and H[lane + 32 (k2 + 16)] from this lane's TMEM table, 4 at a time
+          float2 hlo[4], hhi[4];
+#endif
 #pragma unroll
           for (int k2 = 0; k2 < 16; ++k2) {
+#if KK_TMEM_TABLES
+            if ((k2 & 3) == 0) {
+              tm_ld4(tmem + TM_H + 2 * k2, hlo);
+              tm_ld4(tmem + TM_H + 2 * (k2 + 16), hhi);
+              tm_wait(hhi);
+              asm volatile("" : "+f"(hlo[0].x), "+f"(hlo[0].y), "+f"(hlo[1].x), "+f"(hlo[1].y), "+f"(hlo[2].x),
+                           "+f"(hlo[2].y), "+f"(hlo[3].x), "+f"(hlo[3].y) : "f"(hhi[0].x));
+            }
+            const float2 s0 = c_mul(v[k2], hlo[k2 & 3]);
+            const float2 s1 = c_mul(v[k2 + 16], hhi[k2 & 3]);
+#else
             const float2 s0 = c_mul(v[k2], s_H[lane + 32 * k2]);
             const float2 s1 = c_mul(v[k2 + 16], s_H[lane + 32 * (k2 + 16)]);
+#endif
 #if KK_F32X2
             z[brev(k2, 4)] = add2(make_float2(s0.x, -s0.y), make_float2(s1.x, -s1.y));  // conj -> forward DFT = inverse
 #else
             z[brev(k2, 4)] = make_float2(s0.x + s1.x, -(s0.y + s1.y));  // conj -> forward DFT = inverse
 #endif
           }
-          fft512_pairs(z, lane, scr, s_tw512);
+          fft512_pairs(z, lane, scr, s_tw512, tmem);
           group_sync(gi);  // every tile (warp 3's lies in xs) is done before xs is written
           const int h = lane & 1, r1 = lane >> 1;
           // lane holds window outputs rr = r1 + 16 r2 + 256 h, i.e. positions P = P0 + 2 rr: a
@@ -1168,6 +1216,13 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
   if (!dyn) break;
   }
   flush(prev_s, prev_o);
+#if KK_TMEM_TABLES
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();  // every group is done with the TMEM tables
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "n"(TM_ALLOC) : "memory");
+#endif
 #if KK_PHASE_TIMING
   if (a.dbg) {
     // group totals from the group's thread 0 (wall-clock phases), busy times from every lane 0
@@ -1574,6 +1629,7 @@ cudaError_t launch_unpack12(const uint8_t* src, int16_t* dst, int64_t n_samples,
 // then solved by kk_chol_solve_kernel (one CTA, right-looking Cholesky, fp64).
 // ---------------------------------------------------------------------------
 constexpr int GRAM_T = 16;
+constexpr int CHOL_MAX_N = 256;  // largest static-EQ length the single-CTA solve stages in shared memory
 
 __global__ void __launch_bounds__(256) kk_gram_kernel(const float2* __restrict__ es, int64_t pos_first,
                                                       const float2* __restrict__ sym, int n_count, int ntap,
@@ -1615,8 +1671,9 @@ __global__ void __launch_bounds__(256) kk_gram_kernel(const float2* __restrict__
   }
 }
 
-// (R + ridge * tr(R)/n * I) h = b, R Hermitian positive definite (n <= 256), in place;
-// one CTA of 1024 threads, shared-memory-free (R in global / L2), fp64.  R and b arrive as
+// (R + ridge * tr(R)/n * I) h = b, R Hermitian positive definite (n <= CHOL_MAX_N), in place;
+// one CTA of 1024 threads, fp64; R in global / L2, the pivot column and the right-hand side
+// staged in fixed shared arrays of CHOL_MAX_N entries.  R and b arrive as
 // GRAM_SPLIT partial planes, summed here in a fixed order (deterministic).
 __global__ void __launch_bounds__(1024) kk_chol_solve_kernel(double2* __restrict__ R, double2* __restrict__ b, int n,
                                                              double ridge, float* __restrict__ out) {
@@ -1650,7 +1707,7 @@ __global__ void __launch_bounds__(1024) kk_chol_solve_kernel(double2* __restrict
   __syncthreads();
   // Cholesky R = L L^H (lower triangle overwritten); column k of L staged in shared memory,
   // the trailing update one row per warp (j <= i over the lanes)
-  __shared__ double2 s_col[256];
+  __shared__ double2 s_col[CHOL_MAX_N];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   for (int k = 0; k < n; ++k) {
     const double d = sqrt(R[(int64_t)k * n + k].x);
@@ -1678,7 +1735,7 @@ __global__ void __launch_bounds__(1024) kk_chol_solve_kernel(double2* __restrict
   }
   // forward L y = b, backward L^H h = y: column-oriented substitution, the right-hand side
   // in shared memory, one pivot per step and the n - i remaining updates spread over the CTA
-  __shared__ double2 s_b[256];
+  __shared__ double2 s_b[CHOL_MAX_N];
   for (int i = threadIdx.x; i < n; i += blockDim.x) s_b[i] = b[i];
   __syncthreads();
   for (int i = 0; i < n; ++i) {
@@ -1773,6 +1830,7 @@ cudaError_t launch_frame_sync(const float2* es, int64_t es_first, int L, const u
 
 cudaError_t launch_train_fir(const float2* es, int64_t pos_first, const float2* sym, int n_count, int ntap, double ridge,
                              double2* R, double2* b, float* out, cudaStream_t s) {
+  if (ntap < 1 || ntap > CHOL_MAX_N) return cudaErrorInvalidValue;  // s_col / s_b of kk_chol_solve_kernel
   const int nt = (ntap + GRAM_T - 1) / GRAM_T;
   kk_gram_kernel<<<dim3(nt, nt + 1, GRAM_SPLIT), GRAM_T * GRAM_T, 0, s>>>(es, pos_first, sym, n_count, ntap, R, b);
   cudaError_t e = cudaGetLastError();

@@ -1395,6 +1395,13 @@ extern "C" kk_status kk_rx_set_cspr(kk_rx_t* h, float cspr_db) {
   return KK_OK;
 }
 
+static bool pipeline_idle(const kk_rx_t* h) {
+  if (h->a_deferred >= 0) return false;
+  for (const AsyncSlot& a : h->aslot)
+    if (a.state != 0) return false;
+  return true;
+}
+
 // "batched DC-offset (and CSPR-hypothesis) sweep".  Hypothesis k
 // runs S1-S7 over the same buffers with DC offset dc_values[k] and, if cspr_db_values is
 // given, CSPR cspr_db_values[k] (A_hat = sqrt(d c / (1 + c)), reading R6); the hypotheses go
@@ -1407,11 +1414,14 @@ extern "C" kk_status kk_rx_sweep(kk_rx_t* h, const int16_t* first, int64_t nbuf,
     if (cspr_db_values && !(cspr_db_values[k] > -60.f && cspr_db_values[k] < 60.f))
       return fail(KK_EINVAL, "cspr_db_values out of range");
   }
+  // the caller's submitted-but-unsynced batches would be drained and their counters lost:
+  // like train_fir / frame_sync, the sweep needs an idle streaming pipeline
+  if (!pipeline_idle(h)) return fail(KK_ESTATE, "kk_rx_sync the streaming pipeline first");
   const float dc0 = h->dc;
   const double c0 = h->cspr_lin;
   const int64_t idx0 = h->stream_index;
-  kk_status st = kk_rx_sync(h, nullptr, 0, nullptr);  // start from an empty pipeline
-  if (st != KK_OK) return st;
+  const kk_rx_counts totals0 = h->totals;  // hypothesis passes are not traffic: totals restored below
+  kk_status st = KK_OK;
   for (int k = 0; k < nd; ++k) {
     if (cspr_db_values) h->cspr_lin = std::pow(10.0, (double)cspr_db_values[k] / 10.0);
     kk_rx_set_dc_offset(h, dc_values[k]);
@@ -1425,6 +1435,7 @@ extern "C" kk_status kk_rx_sweep(kk_rx_t* h, const int16_t* first, int64_t nbuf,
   h->cspr_lin = c0;
   kk_rx_set_dc_offset(h, dc0);
   h->stream_index = idx0 + nbuf;
+  h->totals = totals0;
   if (st != KK_OK) return st;
   if (n != (int64_t)nd * nbuf) return fail(KK_ECUDA, "sweep: unexpected result count");
   int kb = 0;
@@ -1461,12 +1472,6 @@ extern "C" kk_status kk_rx_dc_sweep(kk_rx_t* h, const int16_t* first, int64_t nb
 // ---------------------------------------------------------------------------
 // Init-time training (NEXT row of SURVEY 8(f))
 // ---------------------------------------------------------------------------
-static bool pipeline_idle(const kk_rx_t* h) {
-  if (h->a_deferred >= 0) return false;
-  for (const AsyncSlot& a : h->aslot)
-    if (a.state != 0) return false;
-  return true;
-}
 
 // device copy (if needed) of one buffer + halos; returns the device pointer of its sample 0
 static kk_status stage_one(kk_rx_t* h, const int16_t* buffer, int16_t** tmp, const int16_t** dev0) {

@@ -11,6 +11,8 @@ gloo in the CPU tests.
 """
 from __future__ import annotations
 
+import numpy as np
+
 COUNT_KEYS = ("bit_errors", "sym_errors", "bits", "symbols", "clipped_samples", "gated_updates")
 
 
@@ -24,13 +26,61 @@ def shard_range(n_buffers: int, world: int, rank: int):
     return lo, hi
 
 
-def weak_step_buffers(step: int, rank: int, world: int, batch: int, pool: int):
-    """First pool buffer of `rank`'s batch in `step` for a weak-scaling run that
-    cycles a pool of distinct buffers (each rank a different batch per step)."""
-    return (rank * batch + step * batch * world) % pool
+def rank_batches(step: int, rank: int, world: int, batch: int, n_stream: int, scaling: str = "weak"):
+    """The batches (first stream buffer, buffer count) `rank` submits in `step` when a
+    continuous stream of `n_stream` buffers (C5: 4096) is sharded contiguously over `world`
+    ranks (rank r owns shard_range(n_stream, world, r)).
+
+    weak   -- per-GPU work fixed: one batch of up to `batch` consecutive buffers per step,
+              walking the rank's own range in stream order (and wrapping inside it);
+              batches never cross the range end, so ranks never process the same buffer.
+    strong -- total work fixed: a step is one pass over the WHOLE stream, i.e. the rank's
+              range in consecutive batches of up to `batch` buffers."""
+    lo, hi = shard_range(n_stream, world, rank)
+    n = hi - lo
+    if n <= 0 or batch <= 0:
+        return []
+    if scaling == "strong":
+        return [(b, min(batch, hi - b)) for b in range(lo, hi, batch)]
+    if scaling != "weak":
+        raise ValueError(scaling)
+    start = lo + (step * batch) % n
+    return [(start, min(batch, hi - start))]
+
+
+def max_over_ranks(value: float, device=None, group=None) -> float:
+    """all_reduce(MAX) of a per-rank time (the bench's max-over-ranks timing rule)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def comm_info(group=None) -> dict:
+    """The process group the counters are reduced over (logged in the bench line)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return {"backend": None, "world": 1}
+    info = {"backend": str(dist.get_backend(group)), "world": dist.get_world_size(group)}
+    if info["backend"] == "nccl":
+        try:
+            info["nccl_version"] = ".".join(str(x) for x in torch.cuda.nccl.version())
+        except Exception:
+            pass
+    return info
 
 
 def sum_counts(per_buffer):
+    """Sum per-buffer counter dicts (or a structured counter array) into one dict."""
+    if hasattr(per_buffer, "dtype") and getattr(per_buffer.dtype, "names", None):
+        tot = {k: int(per_buffer[k].sum()) for k in COUNT_KEYS}
+        tot["flags"] = int(np.bitwise_or.reduce(per_buffer["flags"])) if len(per_buffer) else 0
+        return tot
     tot = {k: 0 for k in COUNT_KEYS}
     flags = 0
     for c in per_buffer:

@@ -54,8 +54,14 @@ ADC_AA = 2.0e9        # ideal anti-alias at fs/2
 
 def load_constellation(name: str):
     """Read data/constellations/<name>.txt ('<re> <im> <bits>' per line)."""
+    return load_constellation_file(os.path.join(CONST_DIR, name + ".txt"))
+
+
+def load_constellation_file(path: str):
+    """Read a SPEC.md l.89 constellation file ('<re> <im> <label bits>' per line, '#'
+    comments); points scaled to unit mean power, labels parsed as binary strings."""
     pts, labs = [], []
-    with open(os.path.join(CONST_DIR, name + ".txt")) as f:
+    with open(path) as f:
         for line in f:
             line = line.split("#", 1)[0].strip()
             if line:
@@ -231,6 +237,14 @@ def adc_gain(cfg: LinkConfig, i_clean=None):
     return full / (headroom * peak0), nv
 
 
+_GEN_CTX = None  # (cfg, e_clean) inherited by forked generator workers
+
+
+def _noise_worker(seq):
+    cfg, e_clean = _GEN_CTX
+    return _noise_intensity(cfg, e_clean, np.random.Generator(np.random.PCG64(seq)))
+
+
 def make_pool(cfg: LinkConfig, n_pool: int = 1, cache: bool = True, noiseless: bool = False) -> Pool:
     """Generate n_pool distinct buffers of raw ADC codes for cfg.
 
@@ -260,8 +274,19 @@ def make_pool(cfg: LinkConfig, n_pool: int = 1, cache: bool = True, noiseless: b
         intens[:] = i_clean
     else:
         seqs = np.random.SeedSequence(cfg.seed_noise).spawn(n_pool)
-        for b in range(n_pool):
-            intens[b] = _noise_intensity(cfg, e_clean, np.random.Generator(np.random.PCG64(seqs[b])))
+        procs = min(n_pool, os.cpu_count() or 1, int(os.environ.get("KKRX_GEN_PROCS", "16")))
+        if procs > 1 and n_pool >= 4 and cfg.buffer_len >= (1 << 20):
+            # buffers in parallel processes (same per-buffer seeds and arithmetic: identical codes)
+            import multiprocessing as mp
+            global _GEN_CTX
+            _GEN_CTX = (cfg, e_clean)
+            with mp.get_context("fork").Pool(procs) as workers:
+                for b, row in enumerate(workers.imap(_noise_worker, seqs)):
+                    intens[b] = row
+            _GEN_CTX = None
+        else:
+            for b in range(n_pool):
+                intens[b] = _noise_intensity(cfg, e_clean, np.random.Generator(np.random.PCG64(seqs[b])))
     if cfg.adc_bw_hz is not None:
         intens = adc_filter(intens, cfg.adc_bw_hz)
     full = 2 ** (cfg.adc_bits - 1) - 1

@@ -22,20 +22,22 @@ def run_bench(root, *args, timeout):
 
 
 def test_reference_arm_line(root):
-    d = run_bench(root, "--impl", "reference", "--steps", "1", "--warmup", "3", "--ref-workers", "2", timeout=600)
+    d = run_bench(root, "--impl", "reference", "--steps", "1", "--warmup", "3", "--ref-workers", "2", "--pool", "4",
+                  timeout=600)
     assert BASE_KEYS <= set(d)
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["steps"] == 1 and d["warmup"] >= 3 and d["n_gpus"] == 1
     assert d["dtype"] == "f64" and d["data"] == "synthetic" and d["vs_baseline"] is None
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert cb["cpu_model"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
 @pytest.mark.gpu
 def test_kk_arm_line(root):
-    d = run_bench(root, "--steps", "3", "--warmup", "3", "--batch", "16", "--no-cpu-baseline", "--no-cufft",
-                  timeout=900)
+    d = run_bench(root, "--steps", "3", "--warmup", "3", "--batch", "16", "--pool", "16", "--no-cpu-baseline",
+                  "--no-cufft", timeout=900)
     assert BASE_KEYS <= set(d)
     assert d["value"] > 0 and d["dtype"] == "f32" and d["scaling"] == "weak" and d["vs_baseline"] is None
     assert d["config"]["workload"].startswith("C5")
@@ -50,3 +52,6 @@ def test_kk_arm_line(root):
     assert e["value"] <= 1.05 * e["pcie_ceiling"]["value"]
     assert e["value"] < d["value"]
     assert d["errors"]["bits"] > 0
+    # weak scaling over the sharded 4096-buffer stream: 3 steps x 16 buffers, counted from the counters
+    assert d["config"]["buffers_timed"] == 3 * 16 and d["config"]["stream_buffers"] == 4096
+    assert d["comm"]["world"] == 1

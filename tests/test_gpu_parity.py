@@ -424,8 +424,16 @@ def test_dc_offset_sweep():
     d0 = float(pool.dc_offset)
     dvals = [0.7 * d0, d0, 1.3 * d0]
     rx = KKReceiver(cfg.fmt, cfg.buffer_len, cfg.cspr_db, fir, d0, tone_bin=cfg.tbin, ref_pattern=pool.pattern)
+    t0 = rx.totals()
     per_dc, best = rx.dc_sweep(src, off, 2, dvals)
     assert best == 1
+    assert rx.totals() == t0, "hypothesis passes must not count as traffic"
+    # a sweep with submitted-but-unsynced batches is refused (their counters are the caller's)
+    rx.submit_batch(src, off, 2)
+    with pytest.raises(RuntimeError):
+        rx.dc_sweep(src, off, 2, dvals)
+    pend = rx.sync()
+    assert len(pend) == 2
     bers = [c["bit_errors"] / c["bits"] for c in per_dc]
     assert bers[1] <= bers[0] and bers[1] <= bers[2], bers
     ref = KKReceiver(cfg.fmt, cfg.buffer_len, cfg.cspr_db, fir, d0, tone_bin=cfg.tbin, ref_pattern=pool.pattern)
@@ -528,6 +536,38 @@ def test_gmi_matches_oracle():
     o = np.array([shaping.gmi_awgn(p, L[i], 12.0, 10) for i in range(8)])
     assert np.max(np.abs(g - o)) <= 2e-5
     assert g[0] == g.max()  # Gray labelling is the best of these
+
+
+def test_gs_optimiser_loop_on_gpu(tmp_path):
+    """NEXT row 4 end to end: the paper's optimiser loop (perturb one point or
+    swap two labels, keep the move iff the AWGN GMI improves) with ONE candidate per
+    kk_gmi_awgn launch (B = 1, the paper's loop), from 8-QAM at 14 dB.  Its --write output
+    loads through synth.generate.load_constellation_file; the GMI the kernel reports for the
+    result equals oracle.shaping.gmi_awgn to 2e-5 bit; the accepted trace never decreases
+    and ends above 8-QAM's GMI (shaping gain)."""
+    _require_gpu()
+    import importlib.util
+    import os
+    from oracle import shaping
+    from paper_2108_07004_b200 import gmi_awgn
+    from synth.generate import load_constellation, load_constellation_file
+    spec = importlib.util.spec_from_file_location(
+        "gs_optimize_gpu", os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools", "gs_optimize_gpu.py"))
+    gs = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gs)
+    p8, l8 = load_constellation("QAM8")
+    g8 = shaping.gmi_awgn(p8, l8, 14.0, 10)
+    pts, labs, trace = gs.optimize_gpu(p8, l8, 14.0, iters=300, batch=1, seed=8, order=10)
+    assert np.all(np.diff(trace) >= 0)
+    path = tmp_path / "gs8_gpu.txt"
+    gs.write_constellation(str(path), pts, labs, f"GPU GS-8, GMI {trace[-1]:.6f}")
+    p2, l2 = load_constellation_file(str(path))
+    assert np.array_equal(l2, labs)
+    g_gpu = gmi_awgn(p2, l2, 14.0, 10)
+    g_orc = shaping.gmi_awgn(p2, l2, 14.0, 10)
+    assert abs(g_gpu - g_orc) <= 2e-5, (g_gpu, g_orc)
+    assert g_orc > g8, (g_orc, g8)
+    assert abs(g_gpu - trace[-1]) <= 1e-5   # the file holds what the loop accepted
 
 
 def test_pre_kk_equaliser_parity():

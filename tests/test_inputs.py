@@ -3,6 +3,8 @@ synth.generate.pack12 round-trips through an independent bit-level unpacking, fo
 the full 12-bit code range and random streams."""
 import numpy as np
 
+import pytest
+
 from synth.generate import pack12
 
 
@@ -44,3 +46,28 @@ def test_hermgauss_exactness():
             assert abs(np.sum(w * t ** (2 * j + 1))) <= 1e-11 * max(1.0, math.gamma(j + 1.0))
         t0, w0 = np.polynomial.hermite.hermgauss(n)
         assert np.max(np.abs(t - t0)) < 1e-12 and np.max(np.abs(w - w0)) < 1e-12
+
+
+def test_gs_tool_writes_loadable_binary_labels(tmp_path):
+    """tools/gs_optimize_gpu.write_constellation (the GPU optimiser's --write output) writes
+    labels as log2(M)-bit binary strings that synth.generate.load_constellation_file reads
+    back exactly (round-1 ADVICE: it wrote decimal labels the loader parsed as binary)."""
+    import importlib.util
+    import os
+    import numpy as np
+    from synth.generate import load_constellation, load_constellation_file
+    spec = importlib.util.spec_from_file_location(
+        "gs_optimize_gpu", os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools", "gs_optimize_gpu.py"))
+    gs = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gs)
+    rng = np.random.default_rng(5)
+    for name in ("QAM8", "GS128"):
+        p, l = load_constellation(name)
+        perm = rng.permutation(len(p))
+        path = tmp_path / f"{name}.txt"
+        gs.write_constellation(str(path), p, l[perm], "round trip\nsecond header line")
+        p2, l2 = load_constellation_file(str(path))
+        assert np.array_equal(l2, l[perm])
+        assert np.max(np.abs(p2 - p)) < 1e-15
+    with pytest.raises(AssertionError):
+        gs.write_constellation(str(tmp_path / "bad.txt"), p[:3], [0, 1, 1], "not a bijection")

@@ -62,6 +62,56 @@ def propose(rng, pts, labs, sd, sym4, orb, kind):
     return p, l
 
 
+def optimize_gpu(pts, labs, snr_db, iters=300, batch=32, sym4=False, seed=1, step=0.05, order=10):
+    """The paper's perturb/swap loop with `batch` candidate moves per batched
+    kk_gmi_awgn launch (batch = 1: the paper's loop, one move per GMI evaluation).  Returns
+    (points, labels, GMI trace of the accepted baseline, first entry = the start)."""
+    pts = np.asarray(pts, dtype=np.complex128)
+    pts = pts / np.sqrt(np.mean(np.abs(pts) ** 2))
+    labs = np.asarray(labs, dtype=np.int64).copy()
+    rng = np.random.Generator(np.random.PCG64(seed))
+    orb = orbits(pts) if sym4 else None
+    m = len(pts)
+    dmin = np.min(np.abs(pts[:, None] - pts[None, :]) + np.eye(m) * 1e9)
+    sd = step * dmin
+    best = float(np.atleast_1d(gmi_awgn(pts, labs, snr_db, order))[0])
+    trace = [best]
+    stall = 0
+    for it in range(iters):
+        cands = []
+        while len(cands) < batch:
+            # batch = 1 alternates perturbation / swap over the iterations like the oracle loop
+            c = propose(rng, pts, labs, sd, sym4, orb, kind=(len(cands) if batch > 1 else it) % 2)
+            if c is not None:
+                cands.append(c)
+        P = np.stack([c[0] for c in cands])
+        L = np.stack([c[1] for c in cands])
+        g = np.atleast_1d(gmi_awgn(P, L, snr_db, order))
+        k = int(np.argmax(g))
+        if g[k] > best:
+            pts, labs, best = P[k], L[k], float(g[k])
+            stall = 0
+        else:
+            stall += 1
+            if stall % 20 == 0:
+                sd *= 0.5
+        trace.append(best)
+    return pts, labs, np.array(trace)
+
+
+def write_constellation(path, pts, labs, header):
+    """SPEC.md l.89 constellation file: '<re> <im> <label bits>' per point, labels as
+    zero-padded binary strings of log2(M) bits (what synth.generate.load_constellation reads)."""
+    m = len(pts)
+    nbits = int(round(np.log2(m)))
+    assert 1 << nbits == m and sorted(int(x) for x in labs) == list(range(m)), "labels must be a bijection on [0, M)"
+    with open(path, "w") as f:
+        for line in str(header).splitlines():
+            f.write(f"# {line}\n")
+        for p, l in zip(pts, labs):
+            f.write(f"{p.real:+.17e} {p.imag:+.17e} {int(l):0{nbits}b}\n")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--fmt", default="QAM8")
@@ -75,48 +125,19 @@ def main():
     ap.add_argument("--write", default="")
     a = ap.parse_args()
     pts, labs = load_constellation(a.fmt)
-    pts = pts / np.sqrt(np.mean(np.abs(pts) ** 2))
-    rng = np.random.Generator(np.random.PCG64(a.seed))
-    orb = orbits(pts) if a.sym4 else None
-    m = len(pts)
-    dmin = np.min(np.abs(pts[:, None] - pts[None, :]) + np.eye(m) * 1e9)
-    sd = a.step * dmin
-    best = gmi_awgn(pts, labs, a.snr, a.order)
-    g0 = best
     t0 = time.time()
-    trace = [best]
-    stall = 0
-    for it in range(a.iters):
-        cands = []
-        while len(cands) < a.batch:
-            c = propose(rng, pts, labs, sd, a.sym4, orb, kind=len(cands) % 2)
-            if c is not None:
-                cands.append(c)
-        P = np.stack([c[0] for c in cands])
-        L = np.stack([c[1] for c in cands])
-        g = gmi_awgn(P, L, a.snr, a.order)
-        k = int(np.argmax(g))
-        if g[k] > best:
-            pts, labs, best = P[k], L[k], float(g[k])
-            stall = 0
-        else:
-            stall += 1
-            if stall % 20 == 0:
-                sd *= 0.5
-        trace.append(best)
+    pts, labs, trace = optimize_gpu(pts, labs, a.snr, a.iters, a.batch, a.sym4, a.seed, a.step, a.order)
     dt = time.time() - t0
+    g0, best = trace[0], trace[-1]
     ref = {"QAM8": "GS8", "QAM128": "GS128"}.get(a.fmt)
     line = f"{a.fmt} @ {a.snr} dB: GMI {g0:.5f} -> {best:.5f} bits in {a.iters} iterations x {a.batch} candidates, " \
            f"{dt:.1f} s ({a.iters * a.batch / dt:.0f} GMI evaluations/s on the GPU)"
     if ref:
         rp, rl = load_constellation(ref)
-        line += f"; committed {ref}: {gmi_awgn(rp, rl, a.snr, a.order):.5f}"
+        line += f"; committed {ref}: {float(np.atleast_1d(gmi_awgn(rp, rl, a.snr, a.order))[0]):.5f}"
     print(line)
     if a.write:
-        with open(a.write, "w") as f:
-            f.write(f"# GS from tools/gs_optimize_gpu.py {vars(a)}  GMI {best:.6f}\n")
-            for p, l in zip(pts, labs):
-                f.write(f"{p.real:+.17e} {p.imag:+.17e} {int(l)}\n")
+        write_constellation(a.write, pts, labs, f"GS from tools/gs_optimize_gpu.py {vars(a)}  GMI {best:.6f}")
 
 
 if __name__ == "__main__":
