@@ -44,17 +44,27 @@ constexpr size_t SMEM_TW = 1024 * sizeof(float2);     // 1024-pt twiddles
 constexpr size_t SMEM_H = 1024 * sizeof(float2);      // static-EQ spectrum Hs
 constexpr size_t SMEM_TW512 = 512 * sizeof(float2);   // 512-pt twiddles
 constexpr size_t SMEM_LUT = 64 * 64 * sizeof(uint32_t);  // decision table (g <= 64)
+#if KK_TMEM_TABLES
+constexpr size_t SMEM_SHARED = SMEM_LUT;  // the per-lane twiddle / EQ tables live in TMEM (kk_fft.cuh)
+#else
 constexpr size_t SMEM_SHARED = SMEM_TW + SMEM_H + SMEM_TW512 + SMEM_LUT;
+#endif
 constexpr size_t SMEM_EBUF = EBUF * sizeof(float2);
 constexpr size_t SMEM_STG = STG2 * sizeof(int16_t);
 static_assert(SMEM_STG % 16 == 0 && (PKH * 2) % 16 == 0, "bulk copies of the staged codes stay 16-B aligned");
 constexpr size_t SMEM_XS = XS * sizeof(float2);  // also holds the warm-up codes (WARM int16)
 constexpr size_t SMEM_PAT = 832;                 // pattern bytes of one step (768 + alignment)
-constexpr size_t SMEM_GROUP = SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT + 64 + 16;  // + factored WL taps + mbarriers
-constexpr size_t CHAIN_SMEM = SMEM_SHARED + NGROUP * SMEM_GROUP;
-static_assert(SMEM_GROUP % 16 == 0 && SMEM_SHARED % 16 == 0, "16-B aligned regions");
-static_assert(LMS_LUT_G * LMS_LUT_G * 8 + 129 * 8 <= SMEM_SHARED + NGROUP * SMEM_GROUP, "LMS CTAs fit the chain smem");
-static_assert(LMS_LUT_G * LMS_LUT_G * 8 + (2 * 5632 + 16) * 8 + 130 * 8 + 8 <= SMEM_SHARED + NGROUP * SMEM_GROUP,
+constexpr size_t SMEM_GROUP0 = SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT + 64 + 16;  // + factored WL taps + mbarriers
+// + the row-31 pads of the FFT transpose tiles (kk_fft.cuh fft1024): 48 float2 per warp role,
+// the pad placed at the bank offset its tile needs; group regions 128-B aligned
+constexpr size_t SMEM_PADS = NWARPS * 48 * sizeof(float2);
+constexpr size_t SMEM_GROUP = ((SMEM_GROUP0 + 127) / 128) * 128 + SMEM_PADS;
+constexpr size_t SMEM_LMS_NEED = LMS_LUT_G * LMS_LUT_G * 8 + (2 * 5632 + 16) * 8 + 130 * 8 + 8;
+constexpr size_t CHAIN_SMEM0 = SMEM_SHARED + NGROUP * SMEM_GROUP;
+constexpr size_t CHAIN_SMEM = CHAIN_SMEM0 > SMEM_LMS_NEED ? CHAIN_SMEM0 : SMEM_LMS_NEED;  // the LMS CTAs reuse it
+static_assert(SMEM_GROUP % 128 == 0 && SMEM_SHARED % 128 == 0, "128-B aligned regions");
+static_assert(LMS_LUT_G * LMS_LUT_G * 8 + 129 * 8 <= CHAIN_SMEM, "LMS CTAs fit the chain smem");
+static_assert(SMEM_LMS_NEED <= CHAIN_SMEM,
               "warp-per-chain LMS CTAs (table + x2 window + points + mbarrier) fit the chain smem");
 static_assert(WARM2 * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-up codes + tile must fit the x2 window");
 constexpr int WOFF = WARM2 * (int)sizeof(int16_t) / (int)sizeof(float2);  // float2 offset of the warm-up tile in xs
@@ -611,10 +621,17 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     if (a.work_ctr == nullptr) return;
     __syncthreads();
   }
+#if KK_TMEM_TABLES
+  const float2* s_tw = nullptr;     // the per-lane tables are in TMEM (below)
+  const float2* s_tw512 = nullptr;
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem_raw);
+#else
   float2* s_tw = reinterpret_cast<float2*>(smem_raw);
   float2* s_H = reinterpret_cast<float2*>(smem_raw + SMEM_TW);
   float2* s_tw512 = reinterpret_cast<float2*>(smem_raw + SMEM_TW + SMEM_H);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem_raw + SMEM_TW + SMEM_H + SMEM_TW512);
+#endif
+  static_assert(SMEM_SHARED - SMEM_LUT == (KK_TMEM_TABLES ? 0 : SMEM_TW + SMEM_H + SMEM_TW512), "shared table layout");
   // opaque copies: ptxas would otherwise rematerialise these (and the group's smem
   // pointers) from S2R SR_TID.X at every use under register pressure
   const int gi = opaque_i(threadIdx.x / (NWARPS * 32));   // group of this thread
@@ -629,14 +646,17 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
   float2* s_taps = reinterpret_cast<float2*>(gbase + SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT);  // ta[4], tc[4]
   uint64_t* bar = reinterpret_cast<uint64_t*>(gbase + SMEM_EBUF + SMEM_STG + SMEM_XS + SMEM_PAT + 64);
   uint64_t* pbar = bar + 1;
+  float2* pads = reinterpret_cast<float2*>(gbase + ((SMEM_GROUP0 + 127) / 128) * 128);  // transpose-tile row-31 pads
   __shared__ float2 s_pts[128];
   __shared__ uint8_t s_lab[128];
 
+#if !KK_TMEM_TABLES
   for (int k = threadIdx.x; k < 1024; k += blockDim.x) {
     s_tw[k] = a.tw1024[k];
     s_H[k] = a.Hs[k];
   }
   for (int k = threadIdx.x; k < 512; k += blockDim.x) s_tw512[k] = a.tw512[k];
+#endif
   const bool lut_smem = a.lut.g > 0 && a.lut.g <= 64;
   if (lut_smem)
     for (int k = threadIdx.x; k < a.lut.g * a.lut.g; k += blockDim.x) s_lut[k] = a.lut.cell[k];
@@ -909,11 +929,13 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
         float* scr = wt ? wscr
                         : reinterpret_cast<float*>(isH ? ebuf + 256 + 1024 * warp : (warp < 3 ? ebuf + 1024 * warp : xs));
         if (!isH) group_sync(gi);  // all E windows are in registers before ebuf becomes scratch
+        // this warp's row-31 pad at the bank offset of its tile (tile base - 1 mod 16 float2)
+        float2* padp = pads + 48 * warp + ((((smem_u32(scr) >> 3) & 15u) + 15u) & 15u);
         const int nfft = isH ? 2 : 1;
 #pragma unroll 1
         for (int f = 0; f < nfft; ++f) {
           // H tasks: 64-bit transposes through their own 1024-sample output slice
-          fft1024(v, lane, scr, s_tw, tmem, !wt);
+          fft1024(v, lane, scr, s_tw, tmem, !wt, padp);
           if (isH && f == 0) {
             // S2: phi = -H{l} <-> +i sgn(k) L_k (reading R1; the /1024 is in S1), conjugated so the
             // next forward FFT computes the inverse: IFFT(Y) = conj(FFT(conj(Y)))
