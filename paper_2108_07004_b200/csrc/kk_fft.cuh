@@ -273,10 +273,10 @@ __device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __rest
   for (int pass = 0; pass < 2; ++pass) {
     dft_brin<32>(v);
     if (pass == 0) {
-#pragma unroll
 #if KK_TMEM_TABLES
       tm_twiddle<32, 1, 32, 8>(v, tm + TM_TW1024);
 #else
+#pragma unroll
       for (int r = 1; r < 32; ++r) v[r] = c_mul(v[r], tw[r * 32 + lane]);
 #endif
       if (wide) {
@@ -320,10 +320,10 @@ __device__ __forceinline__ void fft512_pairs(float2 (&z)[16], int lane, float* _
   for (int pass = 0; pass < 2; ++pass) {
     dft_brin<16>(z);
     if (pass == 0) {
-#pragma unroll
 #if KK_TMEM_TABLES
       tm_twiddle<16, 1, 16, 4>(z, tm + TM_TW512);
 #else
+#pragma unroll
       for (int r = 1; r < 16; ++r) z[r] = c_mul(z[r], tw512[r * 32 + lane]);
 #endif
 #pragma unroll

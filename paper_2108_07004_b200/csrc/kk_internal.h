@@ -19,7 +19,8 @@ constexpr int WARM = 1536;          // warm-up codes: [3072 i - 1280, 3072 i + 2
 constexpr int PKH = 8;              // extra codes staged per side (pre-KK equaliser reach, <= 8)
 constexpr int STG2 = STG + 2 * PKH;   // staged codes of one step: [3072 i - 256 - PKH, ...)
 constexpr int WARM2 = WARM + 2 * PKH; // staged warm-up codes
-constexpr int XS = 1538;            // x2 window of one step (APPLY): positions 3072 i - 132 + 2 j
+constexpr int XS = 1848;            // x2 window of one step (APPLY, 1538 used): positions 3072 i - 132 + 2 j;
+                                    // pre-KK: the step's 112 padded v' rows (112 x 33 floats) in phase H
 constexpr int NWARPS = 4;          // warps per group
 #ifndef KK_NGROUP
 #define KK_NGROUP 4

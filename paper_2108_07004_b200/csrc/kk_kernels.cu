@@ -26,11 +26,20 @@
 #include "kk_fft.cuh"
 #include "kk_internal.h"
 
+#ifndef KK_S3_UNROLL
+#define KK_S3_UNROLL 2  // S3 output loop unroll (code size vs exposed code-load latency)
+#endif
 #ifndef KK_PHASE_TIMING
 #define KK_PHASE_TIMING 0
 #endif
 
 namespace kk {
+
+constexpr int S3_UNROLL = KK_S3_UNROLL;
+template <int V>
+struct IntC {
+  static constexpr int value = V;
+};
 
 // compile-time phase tag of unrolled loop bodies
 template <int Q>
@@ -70,7 +79,7 @@ static_assert(WARM2 * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-u
 constexpr int WOFF = WARM2 * (int)sizeof(int16_t) / (int)sizeof(float2);  // float2 offset of the warm-up tile in xs
 static_assert(TILE * sizeof(float) <= EQ_KEEP * sizeof(float2), "transpose tile must fit an EQ stride of ebuf");
 static_assert(XS >= 1024 && 3 * 1024 <= STEP, "E-phase 64-bit transpose tiles: three in ebuf[0, STEP), one in xs");
-static_assert(3 * 1024 * sizeof(float) <= SMEM_XS, "pre-KK stash of the three phase-H warps fits the x2 window");
+static_assert((STEP + 512) / 32 * 33 * sizeof(float) <= SMEM_XS, "pre-KK v' rows of a step fit the x2 window");
 
 size_t chain_smem_bytes() { return CHAIN_SMEM; }
 
@@ -302,6 +311,47 @@ __device__ __forceinline__ float2 prek_pair(const ChainArgs& a, const int16_t* s
 #endif
     }
   return acc;
+}
+
+// Pre-KK FIR of a whole step, once per sample: v'[p] for the step's
+// staged positions p in [0, VROWS*32) (position p = owner position sbase + p), row r = 32
+// consecutive positions, one row per lane (rows 28 w .. 28 w + 27 of warp role w), kept in a
+// register sliding window: 48 codes in, 32 outputs, the taps applied in prek_v's order
+// (k ascending from dsum) so each v' is bit for bit prek_v<true>.  Stored padded (row r at
+// vst + 33 r: conflict-free stores; the readers' position lane + 32 j maps to lane + 33 j).
+constexpr int VROWS = (STEP + 512) / 32;  // 112 rows = positions [3072 i - 256, 3072 i + 3328)
+__device__ __forceinline__ void prek_rows(const ChainArgs& a, const int16_t* __restrict__ stg, float* __restrict__ vst,
+                                          int warp, int lane, const Seg& sg) {
+  constexpr int RPW = VROWS / NWARPS;  // 28 rows per warp role
+  static_assert(RPW * NWARPS == VROWS && RPW <= 32, "pre-KK rows per warp");
+  if (lane >= RPW) return;
+  const int r = RPW * warp + lane;
+  float cf[32 + 2 * PKH];
+  // codes of positions 32 r - PKH .. 32 r + 31 + PKH: stg index PKH + p - PKH = 32 r + m
+  const uint4* s4 = reinterpret_cast<const uint4*>(stg + 32 * r);
+#pragma unroll
+  for (int m = 0; m < (32 + 2 * PKH) / 8; ++m) {
+    const uint4 w = s4[m];
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      cf[8 * m + 2 * e] = i16f((int16_t)(ww[e] & 0xffffu));
+      cf[8 * m + 2 * e + 1] = i16f((int16_t)(ww[e] >> 16));
+    }
+  }
+  float acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = sg.prek_dsum;
+#pragma unroll
+  for (int k = -PKH; k <= PKH; ++k)
+    if (k >= -a.prek_h && k <= a.prek_h) {
+      const float g = a.prek[k + PKH];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = fmaf(g, cf[PKH + j - k], acc[j]);
+    }
+  float* dst = vst + 33 * r;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) dst[j] = acc[j];
 }
 
 struct StepPos {
@@ -862,6 +912,12 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
       }
     }
     group_sync(gi);
+    // pre-KK FIR once per sample for the whole step (x2 window = v' rows, free until phase E)
+    float* vst = (PREKK && !warm) ? reinterpret_cast<float*>(xs) : nullptr;
+    if (PREKK && !warm) {
+      prek_rows(a, stg, vst, warp, lane, sg);
+      group_sync(gi);
+    }
 
     KK_DBG(const long long t = clock64(); tdbg[0] += t - tmark; tmark = t)
     // ---- phase 0: Hilbert pairs (warps 0-2, warp 3 = warm-up pair); phase 1: EQ blocks
@@ -890,33 +946,48 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           // S1: l = 0.5 ln(v/d) (the constant 0.5 ln d is in the DC bin, zeroed by the mask)
           c0 = wt ? 6 * i - 2 : 6 * i + 2 * warp;
           const int re0 = (int)(512 * c0 - 256 - base);
-          // pre-KK FIR: S3 needs v' at exactly this lane's j in [8, 40); keep them (x2 window,
-          // free during phase H except for the warm-up task's tiles in warm steps)
-          float* stash = (PREKK && !warm) ? reinterpret_cast<float*>(xs) + 1024 * warp : nullptr;
-          float2 cvp = make_float2(0.f, 0.f);
+          // pre-KK FIR: v' from the step's rows (non-warm steps: window position 1024 w + lane + 32 j
+          // -> padded 1056 w + lane + 33 j), or evaluated here (warm steps, the warm-up task)
+          const float* vrow = (vst && !wt) ? vst + 1056 * warp + lane : nullptr;
+          // one unrolled loop per input mode (0 codes, 1 staged v' rows, 2 v' evaluated here), the
+          // mode chosen once per task: no per-sample branch, no FIR code inside the hot loop
+          auto s1_loop = [&](auto mode_tag) {
+            constexpr int MODE = decltype(mode_tag)::value;
+            float2 cvp = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int j = 0; j < 48; ++j) {
-            const int q = PKH + re0 + lane + 32 * j;
-            // l = lg2(max(code + d, v_min) / d), as max(code/d + 1, v_min/d): one FFMA
-            float lv;
-            if (PREKK) {
-              if ((j & 1) == 0) cvp = prek_pair(a, src, q, sg);  // samples j and j + 1
-              const float cvj = (j & 1) ? cvp.y : cvp.x;
-              if (j >= 8 && j < 40 && stash) stash[32 * (j - 8) + lane] = cvj;
-              lv = fmaxf(cvj, a.vmin) * invd;
-            } else {
-              lv = fmaxf(fmaf((float)src[q], invd, dc_invd), vmin_invd);
-            }
-            // 0.5 ln 2 / 1024 (the 1/1024 of the inverse FFT folded in): applied here, or
-            // (KK_F32X2) by the Hilbert mask multiply, the transform being linear
+            for (int j = 0; j < 48; ++j) {
+              const int q = PKH + re0 + lane + 32 * j;
+              // l = lg2(max(code + d, v_min) / d), as max(code/d + 1, v_min/d): one FFMA
+              float lv;
+              if (MODE == 0) {
+                lv = fmaxf(fmaf((float)src[q], invd, dc_invd), vmin_invd);
+              } else {
+                float cvj;
+                if (MODE == 1) {
+                  cvj = vrow[33 * j];
+                } else {
+                  if ((j & 1) == 0) cvp = prek_pair(a, src, q, sg);  // samples j and j + 1
+                  cvj = (j & 1) ? cvp.y : cvp.x;
+                }
+                lv = fmaxf(cvj, a.vmin) * invd;
+              }
+              // 0.5 ln 2 / 1024 (the 1/1024 of the inverse FFT folded in): applied here, or
+              // (KK_F32X2) by the Hilbert mask multiply, the transform being linear
 #if KK_F32X2
-            const float l = lg2_ftz(lv);
+              const float l = lg2_ftz(lv);
 #else
-            const float l = lg2_ftz(lv) * (0.34657359027997264f / 1024.0f);
+              const float l = lg2_ftz(lv) * (0.34657359027997264f / 1024.0f);
 #endif
-            if (j < 32) v[brev(j, 5)].x = l;        // FFT input registers are bit-reversed
-            if (j >= 16) v[brev(j - 16, 5)].y = l;
-          }
+              if (j < 32) v[brev(j, 5)].x = l;        // FFT input registers are bit-reversed
+              if (j >= 16) v[brev(j - 16, 5)].y = l;
+            }
+          };
+          if (!PREKK)
+            s1_loop(IntC<0>{});
+          else if (vrow)
+            s1_loop(IntC<1>{});
+          else
+            s1_loop(IntC<2>{});
         } else {
 #pragma unroll
           for (int r = 0; r < 32; ++r) v[brev(r, 5)] = ebuf[EQ_KEEP * warp + lane + 32 * r];
@@ -977,28 +1048,38 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           const int16_t* sp0 = src + PKH + s_off + lane + 256;
           float2* dp0 = dst + lane + 256;
           const bool allin = lim >= 1280;  // every output position of this task is < N
-#pragma unroll 2
-          for (int t = 0; t < 16; ++t) {
-            const float2 ph = dp0[32 * t];  // read before output slot m is overwritten below
+          // S3 per input mode (0 codes, 1 staged v' rows, 2 v' evaluated here), chosen once per task
+          auto s3_loop = [&](auto mode_tag) {
+            constexpr int MODE = decltype(mode_tag)::value;
+#pragma unroll S3_UNROLL
+            for (int t = 0; t < 16; ++t) {
+              const float2 ph = dp0[32 * t];  // read before output slot m is overwritten below
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const int o = 32 * t + 512 * hh;
-              const float phi = hh ? -ph.y : ph.x;
-              const float cv = !PREKK ? (float)sp0[o] + sg.dc
-                               : (!warm ? reinterpret_cast<const float*>(xs)[1024 * warp + 32 * (t + 16 * hh) + lane]
-                                        : prek_v<true>(a, sp0, o, sg));
-              const float vv = fmaxf(cv, a.vmin);
-              const float amp = sqrt_ftz(vv);
-              float sp, cp;
-              sincos_small(phi, &sp, &cp);  // |phi| of a few rad at most (KK phase)
+              for (int hh = 0; hh < 2; ++hh) {
+                const int o = 32 * t + 512 * hh;
+                const float phi = hh ? -ph.y : ph.x;
+                const float cv = MODE == 0   ? (float)sp0[o] + sg.dc
+                                 : MODE == 1 ? vst[1056 * warp + 264 + lane + 33 * t + 528 * hh]
+                                             : prek_v<true>(a, sp0, o, sg);
+                const float vv = fmaxf(cv, a.vmin);
+                const float amp = sqrt_ftz(vv);
+                float sp, cp;
+                sincos_small(phi, &sp, &cp);  // |phi| of a few rad at most (KK phase)
 #if KK_F32X2
-              dp0[o] = fma2(make_float2(amp, amp), make_float2(cp, sp), make_float2(-sg.a_hat, 0.f));
+                dp0[o] = fma2(make_float2(amp, amp), make_float2(cp, sp), make_float2(-sg.a_hat, 0.f));
 #else
-              dp0[o] = make_float2(fmaf(amp, cp, -sg.a_hat), amp * sp);
+                dp0[o] = make_float2(fmaf(amp, cp, -sg.a_hat), amp * sp);
 #endif
-              cmin = fminf(cmin, cv);
+                cmin = fminf(cmin, cv);
+              }
             }
-          }
+          };
+          if (!PREKK)
+            s3_loop(IntC<0>{});
+          else if (!warm)
+            s3_loop(IntC<1>{});
+          else
+            s3_loop(IntC<2>{});
           if (cnt && cmin < a.vmin) {
             // rare: some input of this task was clamped -- count exactly (positions < N)
 #pragma unroll 1
@@ -1006,7 +1087,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
               for (int hh = 0; hh < 2; ++hh) {
                 const int o = 32 * t + 512 * hh;
                 const float cv = !PREKK ? (float)sp0[o] + sg.dc
-                                 : (!warm ? reinterpret_cast<const float*>(xs)[1024 * warp + 32 * (t + 16 * hh) + lane]
+                                 : (!warm ? vst[1056 * warp + 264 + lane + 33 * t + 528 * hh]
                                           : prek_v<true>(a, sp0, o, sg));
                 clip += (cv < a.vmin && (allin || lane + 256 + o < lim)) ? 1u : 0u;
               }

@@ -274,10 +274,10 @@ def make_pool(cfg: LinkConfig, n_pool: int = 1, cache: bool = True, noiseless: b
         intens[:] = i_clean
     else:
         seqs = np.random.SeedSequence(cfg.seed_noise).spawn(n_pool)
+        import multiprocessing as mp
         procs = min(n_pool, os.cpu_count() or 1, int(os.environ.get("KKRX_GEN_PROCS", "16")))
-        if procs > 1 and n_pool >= 4 and cfg.buffer_len >= (1 << 20):
+        if procs > 1 and n_pool >= 4 and cfg.buffer_len >= (1 << 20) and not mp.current_process().daemon:
             # buffers in parallel processes (same per-buffer seeds and arithmetic: identical codes)
-            import multiprocessing as mp
             global _GEN_CTX
             _GEN_CTX = (cfg, e_clean)
             with mp.get_context("fork").Pool(procs) as workers:

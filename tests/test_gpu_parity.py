@@ -229,6 +229,46 @@ def test_full_size_c5_bench_launch_config():
     print("C5 full", rep)
 
 
+@pytest.mark.parametrize("name", ["C2", "C4", "C3_QAM8_c8_o10", "C3_GS8_c10_o12", "C3_QAM32_c14_o22"])
+def test_full_size_config_parity(name):
+    """The other BASELINE configs at their stated buffer size (2^22 samples): C2 (16-QAM,
+    one-sided AWGN), C4 (64-QAM at OSNR 28.2 dB, two-sided) and one cell of each C3 format
+    (8-QAM, GS-8, 32-QAM; two-sided).  Buffer 1 of a 2-buffer batch against the oracle:
+    E_s and x2 rel-L2 <= 1e-5 over the whole buffer, taps, decisions outside the exempt
+    set, counters == recount, non-exempt counts == oracle."""
+    _require_gpu()
+    cfg = configs.get(name).link
+    pool = make_pool(cfg, 2)
+    fir = _fir(name)
+    g = _gpu_run(pool, cfg, fir, 2)
+    o = _oracle(g["stream"], g["off"], 1, cfg, pool, fir, g["left"], g["right"])
+    rep = _check_buffer(g, o, 1, cfg, pool)
+    print(name, "full", rep)
+    g["rx"].close()
+
+
+def test_c4_hdfec_threshold_on_gpu():
+    """BASELINE config 4 / PAPER l.85: 64-QAM at OSNR 28.2 dB, CSPR 16 dB crosses the 20 %
+    HD-FEC threshold (Q 6.70 dB).  The GPU chain over 32 distinct full-size
+    two-sided-noise buffers (201 M bits) must reach Q >= 6.70 dB."""
+    _require_gpu()
+    from oracle import metrics as Mx
+    from paper_2108_07004_b200 import KKReceiver, halo_for
+    cfg = configs.get("C4").link
+    nbuf = 32
+    pool = make_pool(cfg, nbuf)
+    left, right = halo_for(cfg.buffer_len)
+    stream, off = make_stream(pool, nbuf, left, right)
+    rx = KKReceiver(cfg.fmt, cfg.buffer_len, cfg.cspr_db, _fir("C4"), pool.dc_offset, tone_bin=cfg.tbin,
+                    ref_pattern=pool.pattern, max_batch=nbuf)
+    c = rx.process_batch(torch.from_numpy(stream).cuda(), off, nbuf, as_array=True)
+    ber = int(c["bit_errors"].sum()) / int(c["bits"].sum())
+    q = float(Mx.q_from_ber(ber))
+    print("C4 GPU: BER", ber, "Q", q)
+    assert q >= Mx.FEC_THRESHOLDS_DB["20%"], q
+    rx.close()
+
+
 def test_empty_and_invalid_calls():
     _require_gpu()
     from paper_2108_07004_b200._lib import KKError
