@@ -154,6 +154,11 @@ kk_status kk_rx_process_batch(kk_rx_t *h, const int16_t *first, int64_t nbuf, ui
  * Memory: the first submission (and any larger nbuf later) allocates the device staging
  * of every pipeline slot at once (tails, taps, counters, labels, and for host or packed
  * input a copy of the batch + halos), so steady-state submits never allocate.
+ * Host input: page-locked memory (cudaHostAlloc / cudaHostRegister / torch pin_memory) is
+ * copied by DMA straight from the caller's buffer; PAGEABLE host memory is first copied by
+ * host threads into a pinned staging buffer of the pipeline slot (allocated once, then
+ * reused) and DMA'd from there, so it keeps the copy/compute overlap at the cost of one host
+ * memcpy (the submit call returns after that memcpy).  kk_rx_pageable_staged counts them.
  * `first` (and the halos) must stay valid and unmodified until kk_rx_sync returns;
  * input written by the caller on the handle's cuda_stream before the call is
  * honoured (stream order).  out_symbols: nbuf*buffer_len/4 bytes (device or host)
@@ -262,6 +267,11 @@ int kk_hermgauss(int order, double *nodes, double *weights);
 
 /* Kernel launches issued by submit/sync since the previous call of this function. */
 int64_t kk_rx_async_launches(kk_rx_t *h);
+
+/* Number of kk_rx_submit_batch calls whose PAGEABLE host input was staged through a pipeline
+ * slot's pinned buffer (see kk_rx_submit_batch); host-only read, never fails for a valid handle.
+ * KK_EINVAL: NULL handle or n. */
+kk_status kk_rx_pageable_staged(const kk_rx_t *h, int64_t *n);
 
 /* Set the stream index of the next buffer (pattern offset = ref_offset +
  * index*buffer_len/4 mod ref_len).  Default after create: 0. */

@@ -83,6 +83,7 @@ EXPORTS = {
     "kk_rx_submit_batch_packed12": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "kk_rx_sync": (C.c_int, [C.c_void_p, C.POINTER(KKCounts), C.c_int64, C.POINTER(C.c_int64)]),
     "kk_rx_async_launches": (C.c_int64, [C.c_void_p]),
+    "kk_rx_pageable_staged": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "kk_rx_set_dc_offset": (C.c_int, [C.c_void_p, C.c_float]),
     "kk_gmi_awgn": (C.c_int, [C.POINTER(C.c_float), C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_double, C.c_int,
                               C.POINTER(C.c_double)]),

@@ -230,7 +230,23 @@ __device__ __forceinline__ int opaque_i(int x) {
 }
 
 // named barrier of one 4-warp group (ids 1..NGROUP; 0 is __syncthreads)
+// KK_JITTER (race hunting, tools/gpu/race_jitter.sh): every warp sleeps a pseudo-random
+// 0..4 us before each group barrier, so warps and groups reach the shared-memory hand-offs
+// in scrambled orders; results must stay bit-identical to the plain build
+#ifndef KK_JITTER
+#define KK_JITTER 0
+#endif
+__device__ __forceinline__ void jitter() {
+#if KK_JITTER
+  unsigned x = (unsigned)clock64() * 2654435761u ^ (threadIdx.x >> 5) * 40503u ^ blockIdx.x * 9973u;
+  x ^= x >> 13;
+  x *= 0x5bd1e995u;
+  x ^= x >> 15;
+  if ((x & 3u) == 0u) __nanosleep(x % 4000u);
+#endif
+}
 __device__ __forceinline__ void group_sync(int gi) {
+  jitter();
   asm volatile("bar.sync %0, %1;" ::"r"(gi + 1), "r"(NWARPS * 32) : "memory");
 }
 

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/kk_rx.h"
@@ -46,6 +47,8 @@ struct AsyncSlot {
   int64_t stage_cap = 0;
   uint8_t* d_pack = nullptr;                // packed-12 input staging [1.5 (left + cap*N + right)]
   int64_t pack_cap = 0;
+  uint8_t* h_pin = nullptr;                 // pinned host staging of PAGEABLE host input (bytes)
+  size_t pin_bytes = 0;
   int64_t nb = 0, index = 0, n_off0 = 0;
   float dc = 0.f, a_hat = 0.f;              // DC offset hypothesis of the batch (kk_rx_set_dc_offset)
   const int16_t* codes = nullptr;           // device samples of buffer 0 of the batch
@@ -103,6 +106,7 @@ struct kk_rx {
   cudaStream_t h2d_stream = nullptr, unpack_stream = nullptr, aux_stream = nullptr;
   cudaEvent_t ev_in = nullptr;
   int64_t a_launches = 0;
+  int64_t a_paged = 0;  // submissions whose pageable host input went through a slot's pinned staging
   DecLut lut{};
   uint8_t *d_lab = nullptr, *d_pattern = nullptr;
   // per-chunk scratch (grown on demand to the largest chunk seen)
@@ -463,6 +467,7 @@ kk_status kk_rx_destroy(kk_rx_t* h) {
     for (void* q : ap)
       if (q) cudaFree(q);
     if (a.h_counts) cudaFreeHost(a.h_counts);
+    if (a.h_pin) cudaFreeHost(a.h_pin);
     for (cudaEvent_t e : {a.ev_done, a.ev_h2d, a.ev_copy, a.ev_zero, a.ev_chain, a.ev_t[0], a.ev_t[1],
                           a.ev_t[2], a.ev_t[3]})
       if (e) cudaEventDestroy(e);
@@ -731,6 +736,37 @@ static bool is_device_ptr(const void* p) {
     return false;
   }
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// host memory the driver would have to stage itself (neither registered/pinned nor device):
+// kk_rx_submit_batch stages it through the slot's pinned buffer instead (page_copy)
+static bool is_pageable_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
+// pageable -> pinned copy on several host threads (one thread copies at ~10 GB/s; the DMA from
+// pinned memory runs at the PCIe rate, ~55 GB/s on the measured B200 host)
+static void page_copy(void* dst, const void* src, size_t bytes) {
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int nt = (int)std::max<size_t>(1, std::min<size_t>({(size_t)(hw ? hw : 1), (size_t)8, bytes >> 24}));
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t chunk = ((bytes + nt - 1) / nt + 63) & ~(size_t)63;
+  for (int k = 0; k < nt; ++k) {
+    const size_t o = (size_t)k * chunk;
+    if (o >= bytes) break;
+    const size_t n = std::min(chunk, bytes - o);
+    th.emplace_back([=] { std::memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, n); });
+  }
+  for (auto& x : th) x.join();
 }
 
 static void fill_chain_common(kk_rx_t* h, ChainArgs& ca, const int16_t* codes_dev) {
@@ -1269,12 +1305,27 @@ static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint
   } else if (in_dev) {
     a.codes = first;
   } else {
-    // host input: pinned (or pageable) -> slot staging on the copy stream.  No wait on the
-    // compute stream: the data is in host memory, and the slot's previous batch has finished
-    // (host wait above), so copies run back to back while earlier batches compute.  The
-    // chain launch that first reads the batch (its tails) waits for this copy.
-    CK(cudaMemcpyAsync(a.d_stage, first - h->left, (size_t)(h->left + nbuf * h->N + h->right) * sizeof(int16_t),
-                       cudaMemcpyHostToDevice, h->h2d_stream));
+    // host input: pinned -> slot staging on the copy stream.  No wait on the compute stream:
+    // the data is in host memory, and the slot's previous batch has finished (host wait
+    // above), so copies run back to back while earlier batches compute.  The chain launch
+    // that first reads the batch (its tails) waits for this copy.  PAGEABLE host memory is
+    // first copied by host threads into the slot's pinned buffer (the slot's previous copy
+    // finished with its chain, waited for above), so the DMA itself is a pinned transfer.
+    const size_t bytes = (size_t)(h->left + nbuf * h->N + h->right) * sizeof(int16_t);
+    const void* src = first - h->left;
+    if (is_pageable_ptr(src)) {
+      if (a.pin_bytes < bytes) {
+        if (a.h_pin) cudaFreeHost(a.h_pin);
+        a.h_pin = nullptr;
+        a.pin_bytes = 0;
+        CK(cudaMallocHost(&a.h_pin, bytes));
+        a.pin_bytes = bytes;
+      }
+      page_copy(a.h_pin, src, bytes);
+      src = a.h_pin;
+      h->a_paged += 1;
+    }
+    CK(cudaMemcpyAsync(a.d_stage, src, bytes, cudaMemcpyHostToDevice, h->h2d_stream));
     CK(cudaEventRecord(a.ev_h2d, h->h2d_stream));
     CK(cudaStreamWaitEvent(h->stream, a.ev_h2d, 0));
     a.codes = a.d_stage + h->left;
@@ -1825,6 +1876,12 @@ extern "C" int64_t kk_rx_async_launches(kk_rx_t* h) {
   const int64_t n = h->a_launches;
   h->a_launches = 0;
   return n;
+}
+
+extern "C" kk_status kk_rx_pageable_staged(const kk_rx_t* h, int64_t* n) {
+  if (!h || !n) return fail(KK_EINVAL, "bad arguments");
+  *n = h->a_paged;
+  return KK_OK;
 }
 
 extern "C" {

@@ -243,6 +243,12 @@ class KKReceiver:
     def async_launches(self):
         return int(self._lib.kk_rx_async_launches(self.h))
 
+    def pageable_staged(self):
+        """kk_rx_pageable_staged: submissions whose pageable host input went through pinned staging."""
+        n = C.c_int64(0)
+        check(self._lib.kk_rx_pageable_staged(self.h, C.byref(n)), "kk_rx_pageable_staged")
+        return int(n.value)
+
     def process(self, stream, offset, out=None):
         return self.process_batch(stream, offset, 1, out)[0]
 

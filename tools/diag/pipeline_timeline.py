@@ -4,7 +4,7 @@ where the per-step time outside the chain launch goes.  python tools/pipeline_ti
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import time  # noqa: E402
 import numpy as np  # noqa: E402

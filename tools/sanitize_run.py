@@ -8,7 +8,7 @@ Exercises every launch shape of the product path on 2^16-sample C2 buffers:
 and checks that the streamed labels equal the synchronous ones (so a sanitizer run that
 perturbs scheduling still has to produce the same result).
 
-usage: python tools/sanitize_run.py [nbig]     (under gpurun, wrapped by compute-sanitizer)
+usage: python tools/sanitize_run.py [nbig] [labels.npy]   (under gpurun; compute-sanitizer or a KK_JITTER build)
 """
 import os
 import sys
@@ -55,6 +55,8 @@ r.sync()
 torch.cuda.synchronize()
 same = bool(torch.equal(out, out_ref))
 print(f"sanitize_run: {nbuf} buffers, streamed == synchronous: {same}", flush=True)
+if len(sys.argv) > 2:  # save the labels to compare builds (tools/gpu/race_jitter.sh)
+    np.save(sys.argv[2], out.cpu().numpy())
 r.close()
 ref.close()
 sys.exit(0 if same else 1)
