@@ -72,6 +72,7 @@ constexpr size_t SMEM_LMS_NEED = LMS_LUT_G * LMS_LUT_G * 8 + (2 * 5632 + 16) * 8
 constexpr size_t CHAIN_SMEM0 = SMEM_SHARED + NGROUP * SMEM_GROUP;
 constexpr size_t CHAIN_SMEM = CHAIN_SMEM0 > SMEM_LMS_NEED ? CHAIN_SMEM0 : SMEM_LMS_NEED;  // the LMS CTAs reuse it
 static_assert(SMEM_GROUP % 128 == 0 && SMEM_SHARED % 128 == 0, "128-B aligned regions");
+static_assert((SMEM_EBUF + SMEM_STG) % 16 == 0, "x2 window 16-B aligned (phase A reads it with 128-bit loads)");
 static_assert(LMS_LUT_G * LMS_LUT_G * 8 + 129 * 8 <= CHAIN_SMEM, "LMS CTAs fit the chain smem");
 static_assert(SMEM_LMS_NEED <= CHAIN_SMEM,
               "warp-per-chain LMS CTAs (table + x2 window + points + mbarrier) fit the chain smem");
@@ -1255,7 +1256,12 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
           const int sidx = tid + NWARPS * 32 * k;
-          const float2 u[4] = {xs[2 * sidx + 3], xs[2 * sidx + 2], xs[2 * sidx + 1], xs[2 * sidx]};
+          // two 128-bit loads (xs[2s], xs[2s+1]) and (xs[2s+2], xs[2s+3]): the warp reads 512
+          // contiguous bytes per load (4 wavefronts, the minimum) instead of 4 strided 64-bit loads
+          const float4 lo = reinterpret_cast<const float4*>(xs)[sidx];
+          const float4 hi = reinterpret_cast<const float4*>(xs)[sidx + 1];
+          const float2 u[4] = {make_float2(hi.z, hi.w), make_float2(hi.x, hi.y), make_float2(lo.z, lo.w),
+                               make_float2(lo.x, lo.y)};
 #if KK_F32X2
           // ta = P, tc = Q here (paired taps): two FFMA2 chains, then one FADD2
           float2 acc0 = mul2(ta[0], make_float2(u[0].x, u[0].x)), acc1 = mul2(ta[1], make_float2(u[1].x, u[1].x));

@@ -561,8 +561,9 @@ def test_init_time_training():
     # within the field tolerance 1e-5.  The taps themselves are compared loosely (2e-3): with
     # ridge 1e-9 the Gram matrix is near-singular along the frequencies where E_s carries no
     # power (75 % of the 4-sps band is outside the signal), and there the LS solution is set
-    # by rounding -- the GPU's fp32 E_s (rel. 5e-7) moves those tap components by up to ~1e-3
-    # without changing the output (measured below), so a tighter tap bound would test rounding.
+    # by rounding -- the GPU's fp32 E_s (rel. 5e-7) moves those tap components (measured on
+    # the B200: output 5.5e-7, taps 1.8e-4) without changing the output, so the tap bound
+    # (1e-3, ~5x the measurement) only guards against a gross error.
     e_s, e0 = train.field_after_s3(st, off, p)
     nn = np.arange(n_first, n_first + n_count)
     A = e_s[4 * nn[:, None] + O.FIR_HALF - np.arange(O.FIR_TAPS)[None, :] - e0]
@@ -571,14 +572,14 @@ def test_init_time_training():
     rel = np.linalg.norm(h_g - h_o) / np.linalg.norm(h_o)
     print("train_fir: output rel", out_rel, "taps rel", rel)
     assert out_rel <= TOL_FIELD, out_rel
-    assert rel < 2e-3, rel
+    assert rel < 1e-3, rel
     # with the fixtures' ridge (1e-4 of the mean Gram diagonal) the near-null directions are
     # pinned and the taps themselves agree closely
     h_g4 = rx.train_fir(src, off, sym[n_first:n_first + n_count], n_first, ridge=1e-4)
     h_o4 = train.train_fir(st, off, p, sym[n_first:n_first + n_count], n_first, n_count, ridge=1e-4)
     rel4 = np.linalg.norm(h_g4 - h_o4) / np.linalg.norm(h_o4)
     print("train_fir ridge 1e-4: taps rel", rel4)
-    assert rel4 <= 1e-4, rel4
+    assert rel4 <= 5e-5, rel4  # measured 5.6e-6
     rx.set_fir(h_g)
     c = rx.process(src, off)
     assert c["bit_errors"] == 0
