@@ -236,7 +236,10 @@ def run_gpu(args):
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
-    if world > 1:
+    # launched by torchrun (any world size, including 1): one NCCL process group, so the
+    # multi-rank code path (barriers, the counter all_reduce, max-over-ranks timing) runs
+    dist_on = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    if dist_on:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         print(f"[bench] rank {rank}/{world} local {local}: process group backend {dist.get_backend()}, "
               f"world {dist.get_world_size()}", file=sys.stderr, flush=True)
@@ -258,7 +261,7 @@ def run_gpu(args):
     # rank 0 generates (and caches) the pool first, then the others load it
     if rank == 0:
         pool = make_pool(cfg, P)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     if rank != 0:
         pool = make_pool(cfg, P)
@@ -298,7 +301,7 @@ def run_gpu(args):
     rx.async_launches()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
@@ -308,7 +311,7 @@ def run_gpu(args):
         counts = rx.sync(as_array=True)  # counters as one array: no per-buffer Python objects in the timed region
         t1.record(cur)
         torch.cuda.synchronize(dev)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     ms = t0.elapsed_time(t1)
     local = sum_counts(counts)
@@ -391,7 +394,7 @@ def run_gpu(args):
                 submit_host(s, packed)
             rx.sync(as_array=True)
             torch.cuda.synchronize(dev)
-            if world > 1:
+            if dist_on:
                 dist.barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -446,7 +449,7 @@ def run_gpu(args):
 
     if rank != 0:
         rx.close()
-        if world > 1:
+        if dist_on:
             dist.destroy_process_group()
         return 0
 
@@ -521,7 +524,7 @@ def run_gpu(args):
                                 "sample": f"{workers} whole 2^22-sample C5 buffers, one per process ({dt:.1f} s)"}
     print(json.dumps(line), flush=True)
     rx.close()
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
     return 0
 

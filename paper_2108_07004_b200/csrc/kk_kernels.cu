@@ -26,6 +26,9 @@
 #include "kk_fft.cuh"
 #include "kk_internal.h"
 
+#ifndef KK_A_ROUNDS
+#define KK_A_ROUNDS 3  // phase A: each thread's 6 symbols in this many rounds (3: -3 % vs 1, code size)
+#endif
 #ifndef KK_S3_UNROLL
 #define KK_S3_UNROLL 2  // S3 output loop unroll (code size vs exposed code-load latency)
 #endif
@@ -651,6 +654,102 @@ template <int MODE>
 __device__ __forceinline__ void lms_warp_body(const LmsArgs& a, unsigned char* lms_smem, float2* s_pts,
                                               uint64_t* s_barp, int c, int lane);
 
+// S5' + S6 + S7 for NS symbols of one step: symbol sidx_k = s0 + sstride k (step-relative,
+// buffer symbol nbase + sidx_k), x2 window xs, factored taps in smem, exact table decision,
+// label store, error counts.  refp: the step's pattern bytes in smem (TMA path) or nullptr
+// (pattern[(pb + sidx) mod P]).
+template <int NS>
+__device__ __forceinline__ void apply_symbols(const ChainArgs& a, int s0, int sstride, int nbase, const float2* xs,
+                                              const float2* s_taps, const uint32_t* s_lut, bool lut_smem,
+                                              const float2* s_pts, const uint8_t* s_lab, uint8_t* outp, bool count_ref,
+                                              const uint8_t* refp, int64_t pb, unsigned& acc_se, unsigned& acc_be) {
+  int refv[NS];
+  if (count_ref) {
+    if (refp) {
+#pragma unroll
+      for (int k = 0; k < NS; ++k) refv[k] = refp[s0 + sstride * k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        int64_t pi = pb + s0 + sstride * k;
+        while (pi >= a.P) pi -= a.P;
+        refv[k] = a.pattern[pi];
+      }
+    }
+  }
+  float2 yv[NS];
+  uint32_t cw[NS];
+  {
+    float2 ta[4], tc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ta[q] = s_taps[q];
+      tc[q] = s_taps[4 + q];
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int sidx = s0 + sstride * k;
+      const float4 lo = reinterpret_cast<const float4*>(xs)[sidx];
+      const float4 hi = reinterpret_cast<const float4*>(xs)[sidx + 1];
+      const float2 u[4] = {make_float2(hi.z, hi.w), make_float2(hi.x, hi.y), make_float2(lo.z, lo.w),
+                           make_float2(lo.x, lo.y)};
+#if KK_F32X2
+      float2 acc0 = mul2(ta[0], make_float2(u[0].x, u[0].x)), acc1 = mul2(ta[1], make_float2(u[1].x, u[1].x));
+      acc0 = fma2(tc[0], make_float2(u[0].y, u[0].y), acc0);
+      acc1 = fma2(tc[1], make_float2(u[1].y, u[1].y), acc1);
+      acc0 = fma2(ta[2], make_float2(u[2].x, u[2].x), acc0);
+      acc1 = fma2(ta[3], make_float2(u[3].x, u[3].x), acc1);
+      acc0 = fma2(tc[2], make_float2(u[2].y, u[2].y), acc0);
+      acc1 = fma2(tc[3], make_float2(u[3].y, u[3].y), acc1);
+      yv[k] = add2(acc0, acc1);
+#else
+      float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
+#pragma unroll
+      for (int t = 0; t < 4; t += 2) {
+        x0 = fmaf(ta[t].x, u[t].x, fmaf(ta[t].y, u[t].y, x0));
+        x1 = fmaf(ta[t + 1].x, u[t + 1].x, fmaf(ta[t + 1].y, u[t + 1].y, x1));
+        y0 = fmaf(tc[t].x, u[t].x, fmaf(tc[t].y, u[t].y, y0));
+        y1 = fmaf(tc[t + 1].x, u[t + 1].x, fmaf(tc[t + 1].y, u[t + 1].y, y1));
+      }
+      yv[k] = make_float2(x0 + x1, y0 + y1);
+#endif
+    }
+  }
+  if (lut_smem) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) cw[k] = s_lut[lut_cell(yv[k], a.lut)];
+  } else {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) cw[k] = (a.lut.g > 0) ? __ldg(a.lut.cell + lut_cell(yv[k], a.lut)) : LUT_BRUTE;
+  }
+  int dk[NS];
+  bool anyb = false;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    dk[k] = decide4(yv[k], cw[k], s_pts);
+    anyb |= (cw[k] & LUT_BRUTE) != 0;
+  }
+  if (__any_sync(0xffffffffu, anyb)) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (cw[k] & LUT_BRUTE) dk[k] = decide_brute(yv[k], s_pts, a.m);
+  }
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    const int sidx = s0 + sstride * k;
+    const int n = nbase + sidx;
+    if (n >= 0 && n < (int)a.n_sym) {
+      const int d = dk[k];
+      const uint8_t ld = s_lab[d];
+      outp[n] = ld;
+      if (count_ref) {
+        acc_se += (refv[k] != d) ? 1u : 0u;
+        acc_be += __popc((unsigned)(ld ^ s_lab[refv[k]]));
+      }
+    }
+  }
+}
+
 // few chains (ChainArgs.lms_warp): one chain per extra CTA, warp 0 runs the
 // warp-per-chain update pass (x2 window in shared memory) after the tails are published
 __device__ __forceinline__ void lms_warp_cta(const LmsArgs& a, unsigned char* smem, int c, int mode) {
@@ -1220,108 +1319,23 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
     }
 
     if (mode == SEG_APPLY) {
-      // ---- S5' + S6 + S7 on symbols [768 i - 32, 768 i + 736) of this owner
+      // ---- S5' + S6 + S7 on symbols [768 i - 32, 768 i + 736) of this owner: each thread's
+      // symbols in KK_A_ROUNDS rounds (code size of the unrolled body vs in-flight symbols)
       const int nbase = SYM_PER_STEP * (int)i - 32;
       const int64_t ko = owner - sg.owner_first;
       uint8_t* outp = sg.out + ko * a.n_sym;
-      constexpr int SPT = SYM_PER_STEP / (NWARPS * 32);  // symbols per thread per step (6)
-      int refv[SPT];
-      if (count_ref) {
-        if (a.pat_tma) {
-          mbar_wait(pbar, pphase);
-          pphase ^= 1u;
-          const int off = (int)(s_pb[gi] & 15);
-#pragma unroll
-          for (int k = 0; k < SPT; ++k) refv[k] = spat[off + tid + NWARPS * 32 * k];
-        } else {
-          const int64_t pb = s_pb[gi];
-#pragma unroll
-          for (int k = 0; k < SPT; ++k) {
-            int64_t pi = pb + tid + NWARPS * 32 * k;
-            while (pi >= a.P) pi -= a.P;
-            refv[k] = a.pattern[pi];
-          }
-        }
+      const uint8_t* refp = nullptr;
+      const int64_t pb = s_pb[gi];
+      if (count_ref && a.pat_tma) {
+        mbar_wait(pbar, pphase);
+        pphase ^= 1u;
+        refp = spat + (int)(pb & 15);
       }
-      float2 yv[SPT];
-      uint32_t cw[SPT];
-      {
-        float2 ta[4], tc[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          ta[q] = s_taps[q];
-          tc[q] = s_taps[4 + q];
-        }
-        // stage 1: y = w^T u + g^T u* with u = (xs[2s+3], xs[2s+2], xs[2s+1], xs[2s]), factored taps
-#pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-          const int sidx = tid + NWARPS * 32 * k;
-          // two 128-bit loads (xs[2s], xs[2s+1]) and (xs[2s+2], xs[2s+3]): the warp reads 512
-          // contiguous bytes per load (4 wavefronts, the minimum) instead of 4 strided 64-bit loads
-          const float4 lo = reinterpret_cast<const float4*>(xs)[sidx];
-          const float4 hi = reinterpret_cast<const float4*>(xs)[sidx + 1];
-          const float2 u[4] = {make_float2(hi.z, hi.w), make_float2(hi.x, hi.y), make_float2(lo.z, lo.w),
-                               make_float2(lo.x, lo.y)};
-#if KK_F32X2
-          // ta = P, tc = Q here (paired taps): two FFMA2 chains, then one FADD2
-          float2 acc0 = mul2(ta[0], make_float2(u[0].x, u[0].x)), acc1 = mul2(ta[1], make_float2(u[1].x, u[1].x));
-          acc0 = fma2(tc[0], make_float2(u[0].y, u[0].y), acc0);
-          acc1 = fma2(tc[1], make_float2(u[1].y, u[1].y), acc1);
-          acc0 = fma2(ta[2], make_float2(u[2].x, u[2].x), acc0);
-          acc1 = fma2(ta[3], make_float2(u[3].x, u[3].x), acc1);
-          acc0 = fma2(tc[2], make_float2(u[2].y, u[2].y), acc0);
-          acc1 = fma2(tc[3], make_float2(u[3].y, u[3].y), acc1);
-          yv[k] = add2(acc0, acc1);
-#else
-          float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
-#pragma unroll
-          for (int t = 0; t < 4; t += 2) {
-            x0 = fmaf(ta[t].x, u[t].x, fmaf(ta[t].y, u[t].y, x0));
-            x1 = fmaf(ta[t + 1].x, u[t + 1].x, fmaf(ta[t + 1].y, u[t + 1].y, x1));
-            y0 = fmaf(tc[t].x, u[t].x, fmaf(tc[t].y, u[t].y, y0));
-            y1 = fmaf(tc[t + 1].x, u[t + 1].x, fmaf(tc[t + 1].y, u[t + 1].y, y1));
-          }
-          yv[k] = make_float2(x0 + x1, y0 + y1);
-#endif
-        }
-      }
-      // stage 2: table words (branch-free cell index; uniform table location)
-      if (lut_smem) {
-#pragma unroll
-        for (int k = 0; k < SPT; ++k) cw[k] = s_lut[lut_cell(yv[k], a.lut)];
-      } else {
-#pragma unroll
-        for (int k = 0; k < SPT; ++k) cw[k] = (a.lut.g > 0) ? __ldg(a.lut.cell + lut_cell(yv[k], a.lut)) : LUT_BRUTE;
-      }
-      // stage 3: decisions from the candidate lists; brute force (off-grid / crowded
-      // cells, or no table) as a rare warp-uniform second pass
-      int dk[SPT];
-      bool anyb = false;
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) {
-        dk[k] = decide4(yv[k], cw[k], s_pts);
-        anyb |= (cw[k] & LUT_BRUTE) != 0;
-      }
-      if (__any_sync(0xffffffffu, anyb)) {
-#pragma unroll
-        for (int k = 0; k < SPT; ++k)
-          if (cw[k] & LUT_BRUTE) dk[k] = decide_brute(yv[k], s_pts, a.m);
-      }
-      // stage 4: labels out, error counts
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) {
-        const int sidx = tid + NWARPS * 32 * k;
-        const int n = nbase + sidx;
-        if (n >= 0 && n < (int)a.n_sym) {
-          const int d = dk[k];
-          const uint8_t ld = s_lab[d];
-          outp[n] = ld;
-          if (count_ref) {
-            acc_se += (refv[k] != d) ? 1u : 0u;
-            acc_be += __popc((unsigned)(ld ^ s_lab[refv[k]]));
-          }
-        }
-      }
+      constexpr int SPT_R = SYM_PER_STEP / (NWARPS * 32) / KK_A_ROUNDS;
+#pragma unroll 1
+      for (int rd = 0; rd < KK_A_ROUNDS; ++rd)
+        apply_symbols<SPT_R>(a, tid + NWARPS * 32 * SPT_R * rd, NWARPS * 32, nbase, xs, s_taps, s_lut, lut_smem, s_pts,
+                             s_lab, outp, count_ref, refp, pb, acc_se, acc_be);
     }
     // keep the last 256 D samples for the next step's first EQ window
     for (int k = tid; k < 256; k += NWARPS * 32) ebuf[k] = ebuf[STEP + k];
