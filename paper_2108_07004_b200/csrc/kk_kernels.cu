@@ -1167,16 +1167,32 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
           // S3 per input mode (0 codes, 1 staged v' rows, 2 v' evaluated here), chosen once per task
           auto s3_loop = [&](auto mode_tag) {
             constexpr int MODE = decltype(mode_tag)::value;
+            // the inputs of output t + 1 (its two codes / v' values and its phase pair) are loaded
+            // during output t, so the shared-memory latency is off the S3 dependency chain
+            auto load_cv = [&](int tt, int hh) -> float {
+              return MODE == 0 ? (float)sp0[32 * tt + 512 * hh] + sg.dc
+                               : MODE == 1 ? vst[1056 * warp + 264 + lane + 33 * tt + 528 * hh]
+                                           : prek_v<true>(a, sp0, 32 * tt + 512 * hh, sg);
+            };
+            float2 ph_n = dp0[0];
+            float cv_n0 = MODE < 2 ? load_cv(0, 0) : 0.f, cv_n1 = MODE < 2 ? load_cv(0, 1) : 0.f;
 #pragma unroll S3_UNROLL
             for (int t = 0; t < 16; ++t) {
-              const float2 ph = dp0[32 * t];  // read before output slot m is overwritten below
+              const float2 ph = ph_n;  // read before output slot m is overwritten below
+              const float cvt[2] = {cv_n0, cv_n1};
+              if (MODE < 2) {
+                const int tn = t < 15 ? t + 1 : 15;
+                ph_n = dp0[32 * tn];
+                cv_n0 = load_cv(tn, 0);
+                cv_n1 = load_cv(tn, 1);
+              } else if (t < 15) {
+                ph_n = dp0[32 * (t + 1)];
+              }
 #pragma unroll
               for (int hh = 0; hh < 2; ++hh) {
                 const int o = 32 * t + 512 * hh;
                 const float phi = hh ? -ph.y : ph.x;
-                const float cv = MODE == 0   ? (float)sp0[o] + sg.dc
-                                 : MODE == 1 ? vst[1056 * warp + 264 + lane + 33 * t + 528 * hh]
-                                             : prek_v<true>(a, sp0, o, sg);
+                const float cv = MODE < 2 ? cvt[hh] : load_cv(t, hh);
                 const float vv = fmaxf(cv, a.vmin);
                 const float amp = sqrt_ftz(vv);
                 float sp, cp;
