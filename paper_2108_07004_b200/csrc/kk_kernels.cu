@@ -301,6 +301,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // sample): 2^23 + 2^22 + c is exact in fp32 for |c| < 2^22, so one IADD and one exact
 // FADD give (float)c bit for bit
 __device__ __forceinline__ float i16f(int16_t c) { return __int_as_float((int)c + 0x4B400000) - 12582912.0f; }
+// int16 code -> float in S1/S3: the exact IADD + FADD form (ALU + FMA pipes) instead of I2F (the
+// quarter-rate XU pipe that also carries the LG2 / SQRT / SIN / COS of S1 and S3); bit-identical
+#ifndef KK_I2F_MAGIC
+#define KK_I2F_MAGIC 1
+#endif
+#if KK_I2F_MAGIC
+#define CODEF(c) i16f(c)
+#else
+#define CODEF(c) ((float)(c))
+#endif
 
 template <bool PREKK>
 __device__ __forceinline__ float prek_v(const ChainArgs& a, const int16_t* src, int q, const Seg& sg) {
@@ -1076,7 +1086,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
               // l = lg2(max(code + d, v_min) / d), as max(code/d + 1, v_min/d): one FFMA
               float lv;
               if (MODE == 0) {
-                lv = fmaxf(fmaf((float)src[q], invd, dc_invd), vmin_invd);
+                lv = fmaxf(fmaf(CODEF(src[q]), invd, dc_invd), vmin_invd);
               } else {
                 float cvj;
                 if (MODE == 1) {
@@ -1170,7 +1180,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
             // the inputs of output t + 1 (its two codes / v' values and its phase pair) are loaded
             // during output t, so the shared-memory latency is off the S3 dependency chain
             auto load_cv = [&](int tt, int hh) -> float {
-              return MODE == 0 ? (float)sp0[32 * tt + 512 * hh] + sg.dc
+              return MODE == 0 ? CODEF(sp0[32 * tt + 512 * hh]) + sg.dc
                                : MODE == 1 ? vst[1056 * warp + 264 + lane + 33 * tt + 528 * hh]
                                            : prek_v<true>(a, sp0, 32 * tt + 512 * hh, sg);
             };
@@ -1218,7 +1228,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
             for (int t = 0; t < 16; ++t)
               for (int hh = 0; hh < 2; ++hh) {
                 const int o = 32 * t + 512 * hh;
-                const float cv = !PREKK ? (float)sp0[o] + sg.dc
+                const float cv = !PREKK ? CODEF(sp0[o]) + sg.dc
                                  : (!warm ? vst[1056 * warp + 264 + lane + 33 * t + 528 * hh]
                                           : prek_v<true>(a, sp0, o, sg));
                 clip += (cv < a.vmin && (allin || lane + 256 + o < lim)) ? 1u : 0u;
