@@ -311,7 +311,7 @@ __device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __rest
 // Forward 512-point DFT of the folded spectrum, one warp:
 //   in : Z[lane + 32*k2] at z[brev4(k2)], k2 in [0,16)   (registers bit-reversed)
 //   out: lane (2*r1 + h) gets z[r2] = X[r1 + 16*(r2 + 16*h)],  X[r] = sum_k Z[k] e^{-2 pi i k r / 512}
-// scr: this warp's tile (>= 16 x 34 floats); tw512[r1*32 + l] = e^{-2 pi i r1 l / 512} (shared).
+// scr: this warp's tile (>= 16 x 34 float2, 8-B aligned); tw512[r1*32 + l] = e^{-2 pi i r1 l / 512} (shared).
 // The inverse transform the method needs is conj(DFT(conj(Z))), done by the caller.
 __device__ __forceinline__ void fft512_pairs(float2 (&z)[16], int lane, float* __restrict__ scr,
                                              const float2* __restrict__ tw512, uint32_t tm) {
@@ -326,17 +326,15 @@ __device__ __forceinline__ void fft512_pairs(float2 (&z)[16], int lane, float* _
 #pragma unroll
       for (int r = 1; r < 16; ++r) z[r] = c_mul(z[r], tw512[r * 32 + lane]);
 #endif
+      // one 64-bit transpose through 16 rows of 34 float2 (row stride = 2 mod 16 bank pairs:
+      // stores of a row and the lanes' (r1, h) reads of column pairs are both conflict-free)
+      float2* s2 = reinterpret_cast<float2*>(scr);
 #pragma unroll
-      for (int r = 0; r < 16; ++r) scr[r * 34 + lane] = z[r].x;
+      for (int r = 0; r < 16; ++r) s2[r * 34 + lane] = z[r];
       __syncwarp();
+      const float2* row = s2 + r1 * 34 + h;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) z[brev(j, 4)].x = scr[r1 * 34 + 2 * j + h];
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < 16; ++r) scr[r * 34 + lane] = z[r].y;
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) z[brev(j, 4)].y = scr[r1 * 34 + 2 * j + h];
+      for (int j = 0; j < 16; ++j) z[brev(j, 4)] = row[2 * j];
       __syncwarp();
     }
   }
