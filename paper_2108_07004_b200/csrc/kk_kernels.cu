@@ -26,6 +26,13 @@
 #include "kk_fft.cuh"
 #include "kk_internal.h"
 
+#ifndef KK_GUIDE_DIV
+#define KK_GUIDE_DIV 4   // guided chunks: remaining steps / (KK_GUIDE_DIV x groups), at most KK_GUIDE_MAX
+                         // (measured: 2 / 256 costs the plain chain 11 %, gains the pre-KK one 2.4 %)
+#endif
+#ifndef KK_GUIDE_MAX
+#define KK_GUIDE_MAX 64
+#endif
 #ifndef KK_A_ROUNDS
 #define KK_A_ROUNDS 3  // phase A: each thread's 6 symbols in this many rounds (3: -3 % vs 1, code size)
 #endif
@@ -941,8 +948,10 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
         c = (unsigned long long)(a.seg[0].i_end - a.seg[0].i_begin);
       } else {
         const int64_t rem = T - (int64_t)seen;
-        int64_t cc = rem / (4 * ngroups);
-        c = (unsigned long long)(cc < 1 ? 1 : (cc > 64 ? 64 : cc));
+        // pre-KK: larger chunks (a warm step -- a chunk start -- evaluates its pre-KK FIR on the fly)
+        constexpr int64_t GDIV = PREKK ? KK_GUIDE_DIV / 2 : KK_GUIDE_DIV, GMAX = PREKK ? 4 * KK_GUIDE_MAX : KK_GUIDE_MAX;
+        int64_t cc = rem / (GDIV * ngroups);
+        c = (unsigned long long)(cc < 1 ? 1 : (cc > GMAX ? GMAX : cc));
       }
       const unsigned long long st = atomicAdd(a.work_ctr, c);
       seen = st + c;
