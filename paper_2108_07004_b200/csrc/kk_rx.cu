@@ -760,12 +760,18 @@ static void page_copy(void* dst, const void* src, size_t bytes) {
   }
   std::vector<std::thread> th;
   const size_t chunk = ((bytes + nt - 1) / nt + 63) & ~(size_t)63;
-  for (int k = 0; k < nt; ++k) {
-    const size_t o = (size_t)k * chunk;
-    if (o >= bytes) break;
-    const size_t n = std::min(chunk, bytes - o);
-    th.emplace_back([=] { std::memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, n); });
+  size_t done = 0;  // bytes handed to threads; the rest (thread creation failed) copied here
+  try {
+    for (int k = 0; k < nt; ++k) {
+      const size_t o = (size_t)k * chunk;
+      if (o >= bytes) break;
+      const size_t n = std::min(chunk, bytes - o);
+      th.emplace_back([=] { std::memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, n); });
+      done = o + n;
+    }
+  } catch (...) {
   }
+  if (done < bytes) std::memcpy(static_cast<uint8_t*>(dst) + done, static_cast<const uint8_t*>(src) + done, bytes - done);
   for (auto& x : th) x.join();
 }
 
