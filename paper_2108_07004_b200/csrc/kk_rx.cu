@@ -18,7 +18,18 @@
 #include <vector>
 
 #include "../../include/kk_rx.h"
+// NVTX ranges around every API call (header-only NVTX v3: free when no tool is attached), so
+// ncu --nvtx / nsys timelines show the receiver's host-side stages (SURVEY.md 5 "NVTX ranges")
+#include <nvtx3/nvToolsExt.h>
 #include "kk_internal.h"
+
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 
 namespace kk {
 int builtin_constellation(int fmt, std::vector<double>& pts, std::vector<int>& labs);
@@ -993,6 +1004,7 @@ static kk_status finish_counts(kk_rx_t* h, int64_t nb, kk_rx_counts* out_per_buf
 
 kk_status kk_rx_process_batch(kk_rx_t* h, const int16_t* first, int64_t nbuf, uint8_t* out_symbols,
                               kk_rx_counts* out_per_buf) {
+  NvtxRange nvtx_range("kk_rx_process_batch");
   if (!h) return fail(KK_EINVAL, "null handle");
   if (h->sticky != KK_OK) return fail(KK_ESTATE, "handle is in a failed state (previous CUDA error)");
   if (!first || nbuf <= 0) return fail(KK_EINVAL, "need a buffer pointer and nbuf > 0");
@@ -1238,6 +1250,7 @@ static kk_status issue_chain(kk_rx_t* h, int p, int t, const LmsArgs* la) {
 enum { IN_INT16 = 0, IN_PACKED12 = 1 };
 
 static kk_status submit_impl(kk_rx_t* h, const void* first_v, int64_t nbuf, uint8_t* out_symbols, int fmt) {
+  NvtxRange nvtx_range("kk_rx_submit_batch");
   const int16_t* first = static_cast<const int16_t*>(first_v);
   const uint8_t* first_b = static_cast<const uint8_t*>(first_v);
   if (!h) return fail(KK_EINVAL, "null handle");
@@ -1406,6 +1419,7 @@ extern "C" kk_status kk_rx_submit_batch_packed12(kk_rx_t* h, const uint8_t* firs
 }
 
 extern "C" kk_status kk_rx_sync(kk_rx_t* h, kk_rx_counts* out_per_buf, int64_t max_out, int64_t* n_out) {
+  NvtxRange nvtx_range("kk_rx_sync");
   if (!h) return fail(KK_EINVAL, "null handle");
   if (h->sticky != KK_OK) return fail(KK_ESTATE, "handle is in a failed state (previous CUDA error)");
   int cur = 0;
@@ -1465,6 +1479,7 @@ static bool pipeline_idle(const kk_rx_t* h) {
 // back to back through the streaming pipeline (each slot carries its own d and A_hat).
 extern "C" kk_status kk_rx_sweep(kk_rx_t* h, const int16_t* first, int64_t nbuf, const float* dc_values,
                                  const float* cspr_db_values, int nd, kk_rx_counts* out_per_hyp, int* best) {
+  NvtxRange nvtx_range("kk_rx_sweep");
   if (!h || !first || !dc_values || nd <= 0 || nbuf <= 0) return fail(KK_EINVAL, "bad arguments");
   for (int k = 0; k < nd; ++k) {
     if (!(dc_values[k] > 0.f)) return fail(KK_EINVAL, "dc_values must be > 0");
@@ -1576,6 +1591,7 @@ static void* iw_get(kk_rx_t* h, int slot, size_t bytes) {
 
 extern "C" kk_status kk_rx_train_fir(kk_rx_t* h, const int16_t* buffer, const float* symbols, int64_t n_first,
                                      int64_t n_count, double ridge, float* out_fir) {
+  NvtxRange nvtx_range("kk_rx_train_fir");
   if (!h || !buffer || !symbols || !out_fir || n_count <= 0) return fail(KK_EINVAL, "bad arguments");
   if (4 * n_first - 101 < 0 || 4 * (n_first + n_count - 1) + 101 >= h->N)
     return fail(KK_EINVAL, "training symbols must satisfy 4*n_first >= 101 and 4*(n_first+n_count-1)+101 < buffer_len");
@@ -1622,6 +1638,7 @@ extern "C" kk_status kk_rx_train_fir(kk_rx_t* h, const int16_t* buffer, const fl
 // chain kernel, then kk_fsync_kernel over every cyclic lag of the pattern.
 extern "C" kk_status kk_rx_frame_sync(kk_rx_t* h, const int16_t* buffer, int64_t n0, int32_t n_corr, int64_t* n_off,
                                       float* peak, double* peak_to_mean) {
+  NvtxRange nvtx_range("kk_rx_frame_sync");
   if (!h || !buffer || !n_off) return fail(KK_EINVAL, "bad arguments");
   if (!h->has_pattern) return fail(KK_EINVAL, "frame synchronisation needs ref_pattern");
   if (n_corr < 16 || n_corr > 8192 || n0 < 0 || 4 * (n0 + (int64_t)n_corr - 1) >= h->N)
@@ -1701,6 +1718,7 @@ extern "C" kk_status kk_rx_set_w_init(kk_rx_t* h, const float* w) {
 // taps after k_steps LMS steps in PILOT mode (known pattern) from the handle's W_init over
 // symbols [0, k_steps) of one buffer (stream position of the handle, as for process).
 extern "C" kk_status kk_rx_train_taps(kk_rx_t* h, const int16_t* buffer, int32_t k_steps, float* out_w) {
+  NvtxRange nvtx_range("kk_rx_train_taps");
   if (!h || !buffer || !out_w || k_steps <= 0) return fail(KK_EINVAL, "bad arguments");
   if (!h->has_pattern) return fail(KK_EINVAL, "PILOT training needs ref_pattern");
   if (4 * (int64_t)k_steps + 16 > h->N) return fail(KK_EINVAL, "k_steps must fit in the buffer");
@@ -1834,6 +1852,7 @@ extern "C" int kk_hermgauss(int order, double* nodes, double* weights) {
 
 extern "C" kk_status kk_gmi_awgn(const float* points, const uint8_t* labels, int m, int n_cand, double snr_db, int order,
                                  double* out_gmi) {
+  NvtxRange nvtx_range("kk_gmi_awgn");
   if (!points || !labels || !out_gmi || m < 2 || m > 256 || (m & (m - 1)) || n_cand < 1 || order < 1 || order > 64)
     return fail(KK_EINVAL, "kk_gmi_awgn: bad arguments (m a power of two <= 256, order 1..64)");
   int nb = 0;
