@@ -258,17 +258,17 @@ __device__ __forceinline__ void dft_brin(float2 (&v)[N]) {
 //   in : x[lane + 32 n2] at v[brev5(n2)]  (lane layout, registers bit-reversed)
 //   out: X[lane + 32 k2] at v[k2]          (lane layout, natural)
 //   X[k] = sum_n x[n] e^{-2 pi i n k / 1024}
-// scr: this warp's 32 x 33 float tile (wide: 32 x 32 float2); tw: shared table tw[r*32 + l] = e^{-2 pi i r l / 1024}.
+// scr: this warp's tile (31 x 33 float2 + pad); tw: shared table tw[r*32 + l] = e^{-2 pi i r l / 1024} (no TMEM).
 // One copy of the 32-point DFT: the two passes are a loop.
 // tm: this warp's TMEM table address (lane quarter, column 0) when KK_TMEM_TABLES.
-// wide: 64-bit transpose through a 32 x 33 float2 tile whose rows 0..30 are scr + 33 r and
-// whose row 31 is `pad` (32 float2 at a bank offset of scr + 1023, i.e. pad = scr - 1 mod 16
+// The transpose goes through a 32 x 33 float2 tile whose rows 0..30 are scr + 33 r and whose
+// row 31 is `pad` (32 float2 at a bank offset of scr + 1023, i.e. pad = scr - 1 mod 16
 // float2): every access is base + immediate (no per-access address arithmetic) and both
 // directions are conflict-free (store: 16 consecutive float2 per half-warp; load at column
 // n: lanes hit banks (l + n) mod 16), so the tile fits the warp's 1024-float2 slice + pad.
 __device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __restrict__ scr,
-                                        const float2* __restrict__ tw, uint32_t tm, bool wide,
-                                        float2* __restrict__ pad = nullptr) {
+                                        const float2* __restrict__ tw, uint32_t tm,
+                                        float2* __restrict__ pad) {
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
     dft_brin<32>(v);
@@ -279,31 +279,15 @@ __device__ __forceinline__ void fft1024(float2 (&v)[32], int lane, float* __rest
 #pragma unroll
       for (int r = 1; r < 32; ++r) v[r] = c_mul(v[r], tw[r * 32 + lane]);
 #endif
-      if (wide) {
-        float2* s2 = reinterpret_cast<float2*>(scr);
+      float2* s2 = reinterpret_cast<float2*>(scr);
 #pragma unroll
-        for (int r = 0; r < 31; ++r) s2[r * 33 + lane] = v[r];
-        pad[lane] = v[31];
-        __syncwarp();
-        const float2* row = (lane < 31) ? s2 + 33 * lane : pad;
+      for (int r = 0; r < 31; ++r) s2[r * 33 + lane] = v[r];
+      pad[lane] = v[31];
+      __syncwarp();
+      const float2* row = (lane < 31) ? s2 + 33 * lane : pad;
 #pragma unroll
-        for (int n = 0; n < 32; ++n) v[brev(n, 5)] = row[n];
-        __syncwarp();
-      } else {
-        // two 32-bit transposes through a padded 32 x 33 float tile
-#pragma unroll
-        for (int r = 0; r < 32; ++r) scr[r * 33 + lane] = v[r].x;
-        __syncwarp();
-#pragma unroll
-        for (int n = 0; n < 32; ++n) v[brev(n, 5)].x = scr[lane * 33 + n];
-        __syncwarp();
-#pragma unroll
-        for (int r = 0; r < 32; ++r) scr[r * 33 + lane] = v[r].y;
-        __syncwarp();
-#pragma unroll
-        for (int n = 0; n < 32; ++n) v[brev(n, 5)].y = scr[lane * 33 + n];
-        __syncwarp();
-      }
+      for (int n = 0; n < 32; ++n) v[brev(n, 5)] = row[n];
+      __syncwarp();
     }
   }
 }

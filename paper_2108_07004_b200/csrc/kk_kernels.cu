@@ -86,7 +86,8 @@ static_assert((SMEM_EBUF + SMEM_STG) % 16 == 0, "x2 window 16-B aligned (phase A
 static_assert(LMS_LUT_G * LMS_LUT_G * 8 + 129 * 8 <= CHAIN_SMEM, "LMS CTAs fit the chain smem");
 static_assert(SMEM_LMS_NEED <= CHAIN_SMEM,
               "warp-per-chain LMS CTAs (table + x2 window + points + mbarrier) fit the chain smem");
-static_assert(WARM2 * sizeof(int16_t) + TILE * sizeof(float) <= SMEM_XS, "warm-up codes + tile must fit the x2 window");
+static_assert(WARM2 * sizeof(int16_t) + 1023 * sizeof(float2) <= SMEM_XS, "warm-up codes + its 31 x 33 float2 tile fit the x2 window");
+static_assert((WARM2 * sizeof(int16_t)) % 8 == 0, "warm-up tile float2-aligned");
 constexpr int WOFF = WARM2 * (int)sizeof(int16_t) / (int)sizeof(float2);  // float2 offset of the warm-up tile in xs
 static_assert(TILE * sizeof(float) <= EQ_KEEP * sizeof(float2), "transpose tile must fit an EQ stride of ebuf");
 static_assert(XS >= 1024 && 3 * 1024 <= STEP, "E-phase 64-bit transpose tiles: three in ebuf[0, STEP), one in xs");
@@ -1141,7 +1142,7 @@ __global__ void __launch_bounds__(NGROUP * NWARPS * 32, 1) kk_chain_kernel(Chain
 #pragma unroll 1
         for (int f = 0; f < nfft; ++f) {
           // H tasks: 64-bit transposes through their own 1024-sample output slice
-          fft1024(v, lane, scr, s_tw, tmem, !wt, padp);
+          fft1024(v, lane, scr, s_tw, tmem, padp);
           if (isH && f == 0) {
             // S2: phi = -H{l} <-> +i sgn(k) L_k (reading R1; the /1024 is in S1), conjugated so the
             // next forward FFT computes the inverse: IFFT(Y) = conj(FFT(conj(Y)))
