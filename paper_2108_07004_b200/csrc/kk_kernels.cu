@@ -324,9 +324,10 @@ template <bool PREKK>
 __device__ __forceinline__ float prek_v(const ChainArgs& a, const int16_t* src, int q, const Seg& sg) {
   if (!PREKK) return (float)src[q] + sg.dc;
   float v = sg.prek_dsum;
-#pragma unroll
-  for (int k = -PKH; k <= PKH; ++k)
-    if (k >= -a.prek_h && k <= a.prek_h) v = fmaf(a.prek[k + PKH], i16f(src[q - k]), v);
+  // rolled: this is the warm-step path only; its unrolled form was ~2.4 k instructions of
+  // cold code beside the hot loops (instruction fetch), the producer prek_rows is the hot one
+#pragma unroll 1
+  for (int k = -a.prek_h; k <= a.prek_h; ++k) v = fmaf(a.prek[k + PKH], i16f(src[q - k]), v);
   return v;
 }
 
@@ -335,19 +336,18 @@ __device__ __forceinline__ float prek_v(const ChainArgs& a, const int16_t* src, 
 // IADDs and one FADD2 (the magic number off both halves) -- bit for bit prek_v<true> twice
 __device__ __forceinline__ float2 prek_pair(const ChainArgs& a, const int16_t* src, int q, const Seg& sg) {
   float2 acc = make_float2(sg.prek_dsum, sg.prek_dsum);
-#pragma unroll
-  for (int k = -PKH; k <= PKH; ++k)
-    if (k >= -a.prek_h && k <= a.prek_h) {
-      const float2 m = make_float2(__int_as_float((int)src[q - k] + 0x4B400000),
-                                   __int_as_float((int)src[q + 32 - k] + 0x4B400000));
+#pragma unroll 1
+  for (int k = -a.prek_h; k <= a.prek_h; ++k) {  // rolled: warm steps only (see prek_v)
+    const float2 m = make_float2(__int_as_float((int)src[q - k] + 0x4B400000),
+                                 __int_as_float((int)src[q + 32 - k] + 0x4B400000));
 #if KK_F32X2
-      const float2 c = add2(m, make_float2(-12582912.0f, -12582912.0f));
-      acc = fma2(make_float2(a.prek[k + PKH], a.prek[k + PKH]), c, acc);
+    const float2 c = add2(m, make_float2(-12582912.0f, -12582912.0f));
+    acc = fma2(make_float2(a.prek[k + PKH], a.prek[k + PKH]), c, acc);
 #else
-      acc.x = fmaf(a.prek[k + PKH], m.x - 12582912.0f, acc.x);
-      acc.y = fmaf(a.prek[k + PKH], m.y - 12582912.0f, acc.y);
+    acc.x = fmaf(a.prek[k + PKH], m.x - 12582912.0f, acc.x);
+    acc.y = fmaf(a.prek[k + PKH], m.y - 12582912.0f, acc.y);
 #endif
-    }
+  }
   return acc;
 }
 
