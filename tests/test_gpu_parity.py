@@ -135,6 +135,40 @@ def test_parity_ragged_buffer_len():
         _check_buffer(g, o, b, cfg, pool)
 
 
+@pytest.mark.parametrize("seed", [11, 22, 33, 44])
+def test_parity_random_links(seed):
+    """Seeded random links beyond the five named configs: any format (square, cross, GS),
+    buffer length a random multiple of 512 (ragged against the 3072-sample step), CSPR
+    6-16 dB, one- or two-sided noise at a random OSNR, random update length K and step mu,
+    static EQ trained in-test on the noiseless twin (oracle.train).  Full
+    parity contract on both buffers of a 2-buffer batch."""
+    _require_gpu()
+    from oracle import train
+    rng = np.random.default_rng(seed)
+    fmt = str(rng.choice(["QAM4", "QAM8", "QAM16", "QAM32", "QAM64", "QAM128", "GS8", "GS128"]))
+    n = 512 * int(rng.integers(64, 161))
+    cspr = float(rng.uniform(6.0, 16.0))
+    osnr = float(rng.uniform(18.0, 36.0))
+    noise = str(rng.choice(["one_sided", "two_sided"]))
+    K = int(rng.choice([512, 1024, 2048]))
+    mu = float(rng.uniform(5e-4, 2e-3))
+    cfg = LinkConfig(fmt, cspr, osnr, noise, n, seed_noise=seed)
+    tr = make_pool(cfg, 1, noiseless=True, cache=False)
+    st0, off0 = make_stream(tr, 1, 2048, 2048)
+    sym = tr.points[tr.pattern.astype(np.int64)]
+    p0 = O.RxParams(buffer_len=n, cspr_db=cspr, dc_offset=tr.dc_offset, fir=np.zeros(O.FIR_TAPS), points=tr.points,
+                    labels=tr.labels, tone_bin=cfg.tbin)
+    nt = min(4096, n // 4 - 64)
+    fir = train.train_fir(st0[: off0 + 4 * nt + 2048], off0, p0, sym[:nt], 0, nt, ridge=1e-4)
+    pool = make_pool(cfg, 2, cache=False)
+    g = _gpu_run(pool, cfg, fir, 2, k_update=K, mu=mu)
+    for b in range(2):
+        o = _oracle(g["stream"], g["off"], b, cfg, pool, fir, g["left"], g["right"], k_update=K, mu=mu)
+        rep = _check_buffer(g, o, b, cfg, pool)
+        print(seed, fmt, n, round(cspr, 1), round(osnr, 1), noise, K, rep)
+    g["rx"].close()
+
+
 @pytest.mark.parametrize("kw", [dict(update_mode=1), dict(sub_block=2048), dict(k_update=1000, mu=2e-3),
                                 dict(update_mode=0, gate_tau=0.0)])
 def test_parity_update_variants(kw):
