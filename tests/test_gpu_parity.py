@@ -138,8 +138,9 @@ def test_parity_ragged_buffer_len():
 @pytest.mark.parametrize("seed", [11, 22, 33, 44])
 def test_parity_random_links(seed):
     """Seeded random links beyond the five named configs: any format (square, cross, GS),
-    buffer length a random multiple of 512 (ragged against the 3072-sample step), CSPR
-    6-16 dB, one- or two-sided noise at a random OSNR, random update length K and step mu,
+    buffer length a random multiple of 512 (ragged against the 3072-sample step), a random
+    tone bin above the signal band, CSPR 6-16 dB, one- or two-sided noise at a random OSNR,
+    random update length K and step mu,
     static EQ trained in-test on the noiseless twin (oracle.train).  Full
     parity contract on both buffers of a 2-buffer batch."""
     _require_gpu()
@@ -152,7 +153,8 @@ def test_parity_random_links(seed):
     noise = str(rng.choice(["one_sided", "two_sided"]))
     K = int(rng.choice([512, 1024, 2048]))
     mu = float(rng.uniform(5e-4, 2e-3))
-    cfg = LinkConfig(fmt, cspr, osnr, noise, n, seed_noise=seed)
+    tone_bin = int(round(n * float(rng.uniform(0.128, 0.14))))  # above the 0.505 GHz (0.12625 fs) band edge
+    cfg = LinkConfig(fmt, cspr, osnr, noise, n, seed_noise=seed, tone_bin=tone_bin)
     tr = make_pool(cfg, 1, noiseless=True, cache=False)
     st0, off0 = make_stream(tr, 1, 2048, 2048)
     sym = tr.points[tr.pattern.astype(np.int64)]
