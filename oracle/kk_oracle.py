@@ -32,6 +32,12 @@ Every function follows one step of the chain described in PAPER.md Sec. 2
 Where the paper is silent the readings R1..R17 of DESIGN.md (= SURVEY.md 8(c)
 items 1-17) are followed; each function names the readings it uses.
 
+Parity unpinned: wl_lms_update's exact tap *trajectory* -- the paper
+fixes neither mu nor the update schedule K, so only properties are pinned (Lipschitz
+bound, ablation, convergence to the Wiener gain SNR/(1+SNR)); the GPU parity tests
+compare the trajectory element by element against this function, not against a paper
+value.
+
 Precision: float64 throughout (numpy), integer phase arithmetic for the tone.
 Library primitives used as single steps: numpy.fft.fft / ifft (S2, one call per
 1024-point block, exactly as the method states it).  No blocking, fusion or

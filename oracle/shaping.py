@@ -11,6 +11,11 @@ iteration, the GMI for the AWGN channel is evaluated and if gains are found,
 the modified constellation is taken as the new baseline."  "Symmetries are added
 to GS-128-QAM to aid convergence."
 
+Parity unpinned: the optimised GS-8 / GS-128 *geometry* that
+optimize() produces -- the paper prints no coordinates; only unit power, bijective
+labels, GMI >= the conventional layout and the Gray 4-QAM recovery are pinned.
+gmi_awgn itself is pinned (Gray 4-QAM = 2 x BPSK AWGN capacity).
+
 GMI: standard BICM generalised mutual information, complex AWGN
 with Es = 1, N0 = 1/SNR, expectation by 2-D Gauss-Hermite quadrature.
 """
